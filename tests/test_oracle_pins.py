@@ -1,0 +1,365 @@
+"""Pins of the CPU oracle against what the paper and mathematics fix (P1-P16).
+
+None of these re-types the oracle's formula: each checks a closed form, an invariant, a textbook value,
+an independent quadrature of a defining integral, a brute-force double sum, or a worked example.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+from scipy import integrate, special
+
+from oracle import fks_oracle as o
+
+L = 13.242640687119286           # (3+√2)R/2 with R = 6
+R = 6.0
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "paper_facts.json")))
+
+
+# ---------------- paper constants (golden) --------------------------------------------------------
+
+def test_paper_constants():
+    assert abs(o.LAMBDA - GOLD["lambda"]["value"]) < 1e-16
+    assert abs(o.support_radius(L) - R) < 1e-13
+    assert abs(L / R - GOLD["box_to_support_ratio"]["value"]) < 1e-15
+    # "96 FFTs per cell at 16 angles": 6 transforms per angle in the paper's scheme
+    assert 6 * 4 * 4 == GOLD["ffts_per_cell_at_16_angles"]["value"]
+    assert o.split_angles(16) == (4, 4) and o.split_angles(32) == (8, 4) and o.split_angles(64) == (8, 8)
+
+
+# ---------------- P1 Gauss-Legendre -----------------------------------------------------------------
+
+def test_P1_gauss_legendre():
+    x, w = o.gauss_legendre(2)
+    assert np.allclose(x, [-1 / math.sqrt(3), 1 / math.sqrt(3)], atol=1e-15) and np.allclose(w, [1, 1], atol=1e-15)
+    x, w = o.gauss_legendre(3)
+    assert np.allclose(x, [-math.sqrt(0.6), 0, math.sqrt(0.6)], atol=1e-15)
+    assert np.allclose(w, [5 / 9, 8 / 9, 5 / 9], atol=1e-15)
+    for n in (4, 8, 16, 32):
+        x, w = o.gauss_legendre(n)
+        for k in range(2 * n):
+            exact = 2.0 / (k + 1) if k % 2 == 0 else 0.0
+            assert abs(np.sum(w * x ** k) - exact) < 1e-14
+    x, w = o.gauss_legendre(16, 0.0, R)       # mapped rule: ∫_0^R ρ^3 = R^4/4
+    assert abs(np.sum(w * x ** 3) - R ** 4 / 4) < 1e-12 * R ** 4
+
+
+# ---------------- P2 direction rules ----------------------------------------------------------------
+
+@pytest.mark.parametrize("nt,nf", [(4, 4), (8, 4), (8, 8), (2, 6)])
+def test_P2_gl_uniform_rule(nt, nf):
+    e, w = o.directions(nt, nf)
+    assert abs(np.sum(w) - 2 * math.pi) < 1e-13                       # half-sphere area
+    assert np.allclose(np.linalg.norm(e, axis=1), 1.0, atol=1e-15)
+    second = np.einsum("d,da,db->ab", w, e, e)
+    assert np.allclose(second, (2 * math.pi / 3) * np.eye(3), atol=1e-13)  # ∫_{S²₊} e_a e_b = (2π/3)δ_ab
+
+
+def test_P2_paper_rule():
+    for nt, nf in [(4, 4), (8, 8)]:
+        e, w = o.directions(nt, nf, o.QUAD_PAPER_RECT)
+        assert abs(np.sum(w) - (math.pi ** 2 / nt) / math.tan(math.pi / (2 * nt))) < 1e-12
+
+
+# ---------------- P3 φ_R and ψ_R against quadrature of their defining integrals ----------------------
+
+@pytest.mark.parametrize("s", [0.0, 0.05, 0.3, 1.7, 3.9, 6.6])
+def test_P3_phi_against_quadrature(s):
+    # φ_R(s) = ∫_{-R}^{R} |ρ| e^{iρs} dρ = 2∫_0^R ρ cos(ρ s) dρ   (reading A1)
+    ref, _ = integrate.quad(lambda r: 2 * r * math.cos(r * s), 0, R, epsabs=1e-14, epsrel=1e-14, limit=400)
+    assert abs(o.phi_R(np.array([s]), R)[0] - ref) <= 1e-13 * R * R
+
+
+@pytest.mark.parametrize("tau", [0.0, 0.07, 0.4, 1.1, 2.5, 6.0])
+def test_P3_psi_against_double_quadrature(tau):
+    # ψ_R(τ) = ∫_0^π φ_R(τ cos θ) dθ with φ_R itself as the ρ-integral (reading A2)
+    inner = lambda th: integrate.quad(lambda r: 2 * r * math.cos(r * tau * math.cos(th)), 0, R,
+                                      epsabs=1e-14, epsrel=1e-14, limit=400)[0]
+    ref, _ = integrate.quad(inner, 0, math.pi, epsabs=1e-13, epsrel=1e-14, limit=400)
+    assert abs(o.psi_R(np.array([tau]), R)[0] - ref) <= 1e-12 * math.pi * R * R
+    if tau == 0.0:
+        assert abs(o.psi_R(np.array([0.0]), R)[0] - math.pi * R * R) < 1e-12
+
+
+def test_P3_radial_gl_reproduces_phi():
+    # 16-point radial GL of the φ integral agrees with the closed form where R|s| ≤ 8 (A6)
+    rho, W = o.gauss_legendre(16, 0.0, R)
+    for s in np.linspace(0, 8 / R, 9):
+        gl = np.sum(2 * W * rho * np.cos(rho * s))
+        assert abs(gl - o.phi_R(np.array([s]), R)[0]) < 1e-12 * R * R
+
+
+# ---------------- P4 / P5: B̂_F assembly and angular convergence -----------------------------------
+
+def test_P4_BF00():
+    for M in (16, 32, 64):
+        tb = o.build_tables(16, L, M=M)
+        c = 7
+        assert abs(o.B_F(tb, (c, c, c), (c, c, c)) - 2 * math.pi ** 2 * R ** 4) < 1e-10 * R ** 4
+
+
+def _BF_closed(xi):
+    # B̂_F(ξ,0) = πR² ∫_{B_R} e^{iξ·x}/|x| dx = 4π²R²(1 − cos R|ξ|)/|ξ|²  (DESIGN.md App. A3)
+    return 4 * math.pi ** 2 * R ** 2 * (1 - math.cos(R * xi)) / xi ** 2
+
+
+def test_P5_angular_convergence():
+    N = 16
+    c = N // 2 - 1
+    l = (c + 1, c + 2, c + 1)          # mode (1, 2, 1), |ξ| = (π/L)√6
+    xi = (math.pi / L) * math.sqrt(6)
+    exact = _BF_closed(xi)
+    errs = []
+    for nt, nf in [(4, 4), (8, 8), (16, 16)]:
+        tb = o.build_tables(N, L, n_theta=nt, n_phi=nf)
+        v_l0 = o.B_F(tb, l, (c, c, c))
+        v_0l = o.B_F(tb, (c, c, c), l)
+        errs.append(max(abs(v_l0 - exact), abs(v_0l - exact)) / abs(exact))
+    assert errs[2] < 1e-9 and errs[1] < 1e-3 and errs[2] < errs[1] < errs[0]
+
+
+# ---------------- P6: fast convolution vs the direct Galerkin double sum (brute force) --------------
+
+@pytest.mark.parametrize("N", [4, 6, 8, 12])
+@pytest.mark.parametrize("kernel", [o.KERNEL_HARD_SPHERES, o.KERNEL_MAXWELL])
+def test_P6_fast_equals_direct(N, kernel):
+    tb = o.build_tables(N, L, M=16, M_r=4, kernel=kernel)
+    rng = np.random.default_rng([1701, N, kernel])
+    for trial in range(3):
+        f = rng.random((N, N, N))
+        if trial == 2:
+            f = 2 * f - 1
+        Qd = o.collision_direct(f, tb)
+        scale = np.abs(Qd).max()
+        for P in (3 * N // 2, 2 * N, 3 * N // 2 - 2):
+            Qf = o.collision_fast(f, tb, P=P)
+            assert np.abs(Qf - Qd).max() <= 1e-12 * scale, (N, P)
+    # an aliased P = N product is a *different* operator when N < 3N/2 − 2: it must not match (A10)
+    if N > 4:
+        Qa = o.collision_fast(f, tb, P=N)
+        assert np.abs(Qa - Qd).max() > 1e-6 * scale
+
+
+def test_P6_fast_equals_direct_N16():
+    N = 16
+    tb = o.build_tables(N, L, M=16)
+    f = np.random.default_rng(5).random((N, N, N))
+    Qd = o.collision_direct(f, tb)
+    assert np.abs(o.collision_fast(f, tb) - Qd).max() <= 1e-12 * np.abs(Qd).max()
+
+
+# ---------------- P7: DFT definition ------------------------------------------------------------------
+
+def test_P7_dft():
+    N = 8
+    c = N // 2 - 1
+    fh = o.forward_modes(np.full((N, N, N), 2.5))
+    assert abs(fh[c, c, c] - 2.5) < 1e-15
+    fh[c, c, c] = 0
+    assert np.abs(fh).max() < 1e-15
+    pm = np.zeros((N, N, N)); pm[3, 1, 6] = 1.0
+    assert np.allclose(np.abs(o.forward_modes(pm)), N ** -3.0, atol=1e-18)
+    # inverse∘forward = identity on K'-band-limited data
+    rng = np.random.default_rng(0)
+    K = N - 1
+    Z = rng.standard_normal((K, K, K)) + 1j * rng.standard_normal((K, K, K))
+    Z = 0.5 * (Z + np.conj(Z[::-1, ::-1, ::-1]))          # Hermitian → real field
+    f = o.inverse_modes(Z, N)
+    assert np.abs(f.imag).max() < 1e-13
+    assert np.abs(o.forward_modes(f.real) - Z).max() < 1e-14 * np.abs(Z).max()
+
+
+# ---------------- P8-P11: mass, realness, bilinearity, symmetries ----------------------------------
+
+@pytest.fixture(scope="module")
+def hs16():
+    return o.build_tables(16, L, M=16)
+
+
+def _two_maxwellian(N, seed):
+    v3 = o.velocity_grid3(N, L)
+    rng = np.random.default_rng(seed)
+    f = np.zeros((N, N, N))
+    for _ in range(2):
+        f += o.maxwellian(v3, rng.uniform(0.5, 1.5), rng.uniform(-1, 1, 3), rng.uniform(0.5, 1.5))
+    f[np.linalg.norm(v3, axis=-1) > R] = 0
+    return f
+
+
+def test_P8_P9_mass_and_realness(hs16):
+    for seed in range(3):
+        f = _two_maxwellian(16, seed)
+        Q, d = o.collision_fast(f, hs16, return_diag=True)
+        ql = o.loss_part(f, hs16)
+        assert abs(Q.sum()) / np.abs(ql).sum() < 1e-11          # Σ_j Q_j = N³Q̂_0 = 0 (App. A4)
+        assert d["max_imag"] <= 1e-13 * np.abs(Q).max()
+        Qp = o.collision_fast(f, hs16, project_mass=True)
+        assert abs(Qp.sum()) / np.abs(ql).sum() < 1e-14
+        assert np.abs(Qp - Q).max() <= 1e-12 * np.abs(Q).max()
+
+
+def test_P10_bilinearity(hs16):
+    f = np.random.default_rng(3).random((16, 16, 16))
+    assert np.abs(o.collision_fast(np.zeros_like(f), hs16)).max() == 0.0
+    Q = o.collision_fast(f, hs16)
+    assert np.abs(o.collision_fast(3 * f, hs16) - 9 * Q).max() <= 1e-14 * 9 * np.abs(Q).max()
+
+
+def test_P11_symmetries(hs16):
+    N = 16
+    f = np.random.default_rng(4).random((N, N, N))
+    Q = o.collision_fast(f, hs16)
+    sc = np.abs(Q).max()
+    # translation by integer grid cells: exact equivariance
+    Qt = o.collision_fast(np.roll(f, (2, -3, 5), axis=(0, 1, 2)), hs16)
+    assert np.abs(Qt - np.roll(Q, (2, -3, 5), axis=(0, 1, 2))).max() <= 1e-13 * sc
+    # reflection v_a → −v_a is j → (N − j) mod N on the node-centred grid (A13)
+    refl = lambda x, ax: np.roll(np.flip(x, axis=ax), 1, axis=ax)
+    for ax in range(3):
+        Qr = o.collision_fast(refl(f, ax), hs16)
+        assert np.abs(Qr - refl(Q, ax)).max() <= 1e-12 * sc
+    # swap vx ↔ vy is a symmetry of the GL × uniform-φ rule with even n_φ
+    Qs = o.collision_fast(np.swapaxes(f, 0, 1), hs16)
+    assert np.abs(Qs - np.swapaxes(Q, 0, 1)).max() <= 1e-12 * sc
+
+
+# ---------------- P12: equilibrium, spectral accuracy ------------------------------------------------
+
+def test_P12_equilibrium():
+    ratios = []
+    for N in (16, 24, 32):
+        tb = o.build_tables(N, L, M=16)
+        v3 = o.velocity_grid3(N, L)
+        f = o.maxwellian(v3, 1.0, (0.3, -0.2, 0.1), 1.0)
+        f[np.linalg.norm(v3, axis=-1) > R] = 0
+        ratios.append(np.abs(o.collision_fast(f, tb)).max() / np.abs(o.loss_part(f, tb)).max())
+    assert ratios[0] > ratios[1] > ratios[2]
+    assert ratios[2] < 2e-3          # measured 4.7e-4 (u = 0); spectral tail at N = 32
+
+
+# ---------------- P13: absolute constants via the loss rate -----------------------------------------
+
+def test_P13_loss_rate_hard_spheres():
+    N = 32
+    tb = o.build_tables(N, L, M=64)                  # 8 × 8
+    v3 = o.velocity_grid3(N, L)
+    f = o.maxwellian(v3, 1.0, (0, 0, 0), 1.0)
+    f[np.linalg.norm(v3, axis=-1) > R] = 0
+    i = N // 2
+    nu = o.loss_part(f, tb)[i, i, i] / f[i, i, i]
+    assert abs(nu / GOLD["hard_sphere_loss_rate"]["value_rho1_T1"] - 1) < 2e-4
+
+
+def test_P13_loss_rate_maxwell():
+    N = 24
+    tb = o.build_tables(N, L, M=64, M_r=16, kernel=o.KERNEL_MAXWELL)
+    v3 = o.velocity_grid3(N, L)
+    f = o.maxwellian(v3, 1.0, (0, 0, 0), 1.0)
+    f[np.linalg.norm(v3, axis=-1) > R] = 0
+    i = N // 2
+    nu = o.loss_part(f, tb)[i, i, i] / f[i, i, i]
+    assert abs(nu - GOLD["maxwell_loss_rate"]["value_rho1"]) < 1e-3
+
+
+# ---------------- P14: BKW exact solution (Maxwell molecules) ----------------------------------------
+
+def test_P14_bkw_closed_form_consistency():
+    # the analytic ∂f/∂t used below agrees with a finite difference in K and with its Fourier form
+    v3 = o.velocity_grid3(16, L)
+    K, h = 0.7, 1e-6
+    fd = (o.bkw(v3, K + h) - o.bkw(v3, K - h)) / (2 * h) * (1 - K) / 6
+    assert np.abs(fd - o.bkw_dfdt(v3, K)).max() < 1e-8
+    # Fourier: F[f_K](ξ) = e^{-K|ξ|²/2}(1 − (1−K)|ξ|²/2), F[∂_t f](ξ) = (1−K)²|ξ|⁴e^{-K|ξ|²/2}/24 (App. A6)
+    xi = 0.9
+    r = np.linspace(0, 12, 20001)
+    ft = lambda g: 4 * math.pi * np.trapezoid(g * r * r * np.sinc(xi * r / math.pi), r)
+    r3 = np.stack([r, 0 * r, 0 * r], -1)
+    assert abs(ft(o.bkw(r3, K)) - math.exp(-K * xi * xi / 2) * (1 - (1 - K) * xi * xi / 2)) < 1e-7
+    assert abs(ft(o.bkw_dfdt(r3, K)) - (1 - K) ** 2 * xi ** 4 * math.exp(-K * xi * xi / 2) / 24) < 1e-7
+
+
+def test_P14_bkw_N48():
+    N = 48
+    v3 = o.velocity_grid3(N, L)
+    K = 0.7
+    f = o.bkw(v3, K)
+    f[np.linalg.norm(v3, axis=-1) > R] = 0
+    Q = o.collision_fast_streamed(f, dict(L=L, M=64, M_r=16, kernel=o.KERNEL_MAXWELL))
+    ex = o.bkw_dfdt(v3, K)
+    assert np.abs(Q - ex).max() / np.abs(ex).max() < 1e-3           # measured 3.2e-4
+
+
+@pytest.mark.slow
+def test_P14_bkw_N64_1e6():
+    """BJ.north_star: '∂f/∂t matches Q to 1e-6' — reachable at N = 64, 8×8, M_r = 16, K = 0.7 (~45 s)."""
+    if os.environ.get("FKS_SKIP_SLOW"):
+        pytest.skip("FKS_SKIP_SLOW set")
+    N = 64
+    v3 = o.velocity_grid3(N, L)
+    K = 0.7
+    f = o.bkw(v3, K)
+    f[np.linalg.norm(v3, axis=-1) > R] = 0
+    Q = o.collision_fast_streamed(f, dict(L=L, M=64, M_r=16, kernel=o.KERNEL_MAXWELL))
+    ex = o.bkw_dfdt(v3, K)
+    assert np.abs(Q - ex).max() / np.abs(ex).max() < 1e-6            # measured 3.65e-7
+
+
+# ---------------- P15: transport -----------------------------------------------------------------------
+
+def test_P15_worked_cases():
+    # SPEC S:265-267 cases under the half-open rule (A16).  N = 10, c = 1: k = 8 moves 0.6 cell.
+    cell = o.GenericCell(N=10, c_num=1, c_den=1)
+    d = cell.advance()
+    case = GOLD["transport_worked_cases"]["cases"][0]
+    assert d[0, 8] == case["delta"] and cell.offsets[0, 8] / 10 == case["new_offset_cells"]
+    assert d[0, 5] == 0 and cell.offsets[0, 5] == 0                    # v = 0 stays (case 3)
+    # N = 4, c = 2: k = 3 moves exactly one cell; start at offset −½ cell
+    cell = o.GenericCell(N=4, c_num=2, c_den=1)
+    cell.offsets[:, 3] = -2
+    d = cell.advance()
+    case = GOLD["transport_worked_cases"]["cases"][1]
+    assert d[0, 3] == case["delta"] and cell.offsets[0, 3] / 4 == case["new_offset_cells"]
+
+
+def test_P15_exact_periodicity():
+    # c = 1, N = 32: index k moves (2k − 32)/32 cell per step; after 32 steps exactly 2k − 32 cells
+    N = 32
+    cell = o.GenericCell(N=N, c_num=1, c_den=1)
+    tot = np.zeros((3, N), dtype=np.int64)
+    for _ in range(N):
+        tot += cell.advance()
+    assert np.array_equal(tot[0], 2 * np.arange(N) - N) and not cell.offsets.any()
+    cell = o.GenericCell(N=N, c_num=1, c_den=8)
+    for _ in range(100):
+        cell.advance()
+        assert (cell.offsets >= -N * 8 // 2).all() and (cell.offsets < N * 8 // 2).all()
+
+
+def test_P15_transport_permutation():
+    N, shape = 4, (3, 2, 5)
+    n = 30
+    f = np.random.default_rng(9).random((n, N, N, N))
+    cell = o.GenericCell(N=N, c_num=7, c_den=3)
+    d1 = cell.advance(); d2 = cell.advance()
+    g = o.transport(o.transport(f, shape, d1), shape, d2)
+    assert np.array_equal(g, o.transport(f, shape, d1 + d2))           # composition
+    assert np.allclose(g.sum(axis=0), f.sum(axis=0), rtol=0, atol=1e-14)  # per-velocity mass
+    assert np.array_equal(np.sort(g, axis=0), np.sort(f, axis=0))      # a permutation per velocity
+    for j in (0, 7, 29):
+        src = o.source_cells(j, shape, d1)
+        ref = np.take_along_axis(f.reshape(n, -1), src.reshape(1, -1), 0).reshape(N, N, N)
+        assert np.array_equal(o.transport(f, shape, d1)[j], ref)
+
+
+# ---------------- P16: Euler ---------------------------------------------------------------------------
+
+def test_P16_euler(hs16):
+    f = _two_maxwellian(16, 7)[None]
+    cell = o.GenericCell(N=16, c_num=0, c_den=1)
+    assert np.array_equal(o.fks_step(f, (1, 1, 1), cell, hs16, 0.0), f)
+    Q = o.collision_fast(f[0], hs16)
+    g1 = o.fks_step(f, (1, 1, 1), cell, hs16, 0.01)
+    g2 = o.fks_step(f, (1, 1, 1), cell, hs16, 0.02)
+    assert np.abs((g2 - f) - 2 * (g1 - f)).max() < 1e-15 and np.abs(g1[0] - f[0] - 0.01 * Q).max() < 1e-16
