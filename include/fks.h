@@ -1,0 +1,128 @@
+/* fks.h — C ABI of libfks: the hot path of the Fast Kinetic Scheme for the 3D/3D Boltzmann equation
+ * (J. Narski, arXiv 1701.01608) on one NVIDIA B200 (sm_100a), fp64.
+ *
+ * Citations: "P:n" = line n of the paper's PAPER.md; "A<n>" = the readings of garbled or silent passages
+ * listed in DESIGN.md §3.  What the calls compute is defined in DESIGN.md §2; in short, per spatial cell j,
+ *
+ *   f^_l  = N^-3 sum_j f_j e^{-2 pi i l.j/N},   l in K'^3,  K' = {-(N/2-1), ..., N/2-1}
+ *   Q^_k  = sum_{l,m in K', l+m=k} beta(l,m) f^_l f^_m,  beta(l,m) = sum_{t=0..T} a_t(l) b_t(m)  (Eq. CF1)
+ *   Q_j   = sum_{k in K'} Q^_k e^{2 pi i k.j/N}
+ *
+ * with the separated Carleman weights a_t, b_t of Appendix A (hard spheres B~ = 1, or Maxwell
+ * molecules by a radial split, A6) and the loss term t = 0 (a_0 = 1, b_0 = -sum_{t>=1} a_t b_t).
+ *
+ * Conventions (all calls):
+ *  - Arrays f, Q, f_in, f_out are DEVICE pointers to fp64, owned by the caller, layout [n_cells][N][N][N]
+ *    C order (kz fastest); the velocity node (kx,ky,kz) is v = -L + (kx,ky,kz)*2L/N (A13).  Spatial cell
+ *    index for transport is (jx*ny + jy)*nz + jz on a periodic nx*ny*nz grid (A21).
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream); every call is stream-ordered
+ *    and asynchronous unless stated.  No exception crosses the ABI.
+ *  - Validation errors return before any launch.  Asynchronous kernel faults surface as FKS_ERR_CUDA on the
+ *    next call or on fks_sync.  fks_last_error() returns a thread-local message for the last failure.
+ *  - A handle is used from one host thread at a time.  Tables are immutable after init.
+ *  - Inputs and outputs must not overlap (checked by pointer range): FKS_ERR_INVALID.
+ *  - There is no CPU fallback: without a CUDA device every compute call returns FKS_ERR_CUDA.
+ */
+#ifndef FKS_H
+#define FKS_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct fks_ctx fks_ctx;
+
+typedef enum {
+  FKS_OK = 0,
+  FKS_ERR_INVALID = 1,      /* bad argument, overlapping buffers, host pointer where a device pointer is needed */
+  FKS_ERR_UNSUPPORTED = 2,  /* N odd, N < 4, N > 64, P < 3N/2-2, unknown kernel/rule, requested path unavailable */
+  FKS_ERR_NOMEM = 3,        /* device allocation failed */
+  FKS_ERR_CUDA = 4,         /* launch failure or asynchronous CUDA error (sticky errors stay sticky) */
+  FKS_ERR_STATE = 5         /* e.g. fks_transport_step / fks_step before fks_transport_setup */
+} fks_status;
+
+typedef enum {
+  FKS_KERNEL_HARD_SPHERES = 0,  /* B~ = 1          (B = |u|/4, A4)                 */
+  FKS_KERNEL_MAXWELL = 1        /* B~ = (1/pi)(|x|^2+|y|^2)^(-1/2)  (B = 1/(4 pi); Eq. Btilde_pl, A5) */
+} fks_kernel;
+
+typedef enum {
+  FKS_QUAD_GL_UNIFORM = 0,  /* default: Gauss-Legendre in cos(theta) x uniform phi on the half sphere (A11) */
+  FKS_QUAD_PAPER_RECT = 1   /* (theta_p, phi_q) = (p pi/A1, q pi/A2), weight pi^2/(A1 A2) sin(theta_p) (A2) */
+} fks_quad;
+
+typedef enum {
+  FKS_PATH_AUTO = 0,        /* fastest instantiated path for (N, P) */
+  FKS_PATH_GENERIC = 1,     /* per-axis DFT kernels through device workspace, any even N in [4, 64]     */
+  FKS_PATH_FAST = 2         /* fused pruned-FFT kernels (N = 32, P = 48); FKS_ERR_UNSUPPORTED elsewhere */
+} fks_path;
+
+typedef struct {
+  int N;                        /* velocity points per axis, even, 4..64                                   */
+  double L;                     /* half-width of the periodic velocity box [-L, L)^3; support R = lambda*L  */
+  int M_angles;                 /* number of half-sphere directions (A12: n_theta = 2^ceil(log2(M)/2))      */
+  int M_radial;                 /* Maxwell molecules: radial GL nodes on [0, R_c] (>= 1); HS: unused       */
+  int kernel;                   /* fks_kernel                                                              */
+  int n_theta, n_phi;           /* 0,0 = derive from M_angles (A12)                                        */
+  int quad_rule;                /* fks_quad                                                                */
+  int pad;                      /* 0 = P = 3N/2 (default, A10); else explicit P >= 3N/2 - 2                */
+  double cutoff_ratio;          /* Carleman cutoff R_c = ratio*R; 0 or 1 = paper-literal (A7), max 1.7072  */
+  int project_mass;             /* 1 = set Q^_0 := 0 exactly (A24); default 0                              */
+  long long max_cells_in_flight;/* workspace limit in cells per chunk; 0 = auto                            */
+  int path;                     /* fks_path                                                                */
+} fks_params;
+
+/* Precompute the separated-kernel weight tables a_t, b_t (t = 0..T) on the device (A1-A7).
+ * T = M_angles (hard spheres) or M_angles*M_radial (Maxwell molecules).  *out receives the handle (owned by
+ * the caller; release with fks_destroy).  Defaults: paper-literal cutoff, GL x uniform rule, P = 3N/2. */
+fks_status fks_collision_init(fks_ctx** out, int N, double L, int M_angles, int M_radial, int kernel);
+fks_status fks_collision_init_ex(fks_ctx** out, const fks_params* p);
+
+/* Q[c] = Q(f[c], f[c]) for c < n_cells (device pointers, [n_cells][N][N][N] fp64).  n_cells = 0: no-op.
+ * Q must not overlap f. */
+fks_status fks_collision_batch(fks_ctx* h, const double* f, double* Q, long long n_cells, void* stream);
+
+/* Same operation on HOST buffers: copies f to the device, computes, copies Q back, in chunks; returns when
+ * Q is written (synchronous).  Used for the end-to-end measurement. */
+fks_status fks_collision_batch_host(fks_ctx* h, const double* f_host, double* Q_host, long long n_cells);
+
+/* Configure the exact transport (A16): periodic nx*ny*nz cells of width dx, time step
+ * dt = (cfl_num/cfl_den)*dx/L (rational CFL c = dt*L/dx), generic-cell offsets reset to 0 (cell centres).
+ * cfl_num = 0 makes transport the identity (space-homogeneous runs).  cfl_den >= 1. */
+fks_status fks_transport_setup(fks_ctx* h, int nx, int ny, int nz, long long cfl_num, long long cfl_den);
+
+/* One exact transport step: advances the generic-cell offsets (host, O(N)) and gathers
+ * f_out[j][k] = f_in[(j - delta(k)) mod (nx,ny,nz)][k] (bit-exact permutation).  f_out must not overlap f_in. */
+fks_status fks_transport_step(fks_ctx* h, const double* f_in, double* f_out, void* stream);
+
+/* One FKS time step (Eq. disc_relax; A17, A18): transport, then collision, then explicit
+ * Euler: f_out = f* + coll_scale * Q(f*), f* = transported f_in, coll_scale = dt/Kn. */
+fks_status fks_step(fks_ctx* h, const double* f_in, double* f_out, double coll_scale, void* stream);
+
+/* Host-buffer variant of fks_step (synchronous), for the end-to-end measurement. */
+fks_status fks_step_host(fks_ctx* h, const double* f_in_host, double* f_out_host, double coll_scale);
+
+/* Diagnostics: padded size P, number of separated terms T (the loss term t = 0 is extra), cutoff R_c,
+ * lambda = 2/(3+sqrt 2).  Any out pointer may be NULL. */
+fks_status fks_get_info(const fks_ctx* h, int* P, int* T, double* R, double* lambda);
+
+/* Test-only: copy the tables to host arrays a_host, b_host [(T+1)][N-1][N-1][N-1], the directions
+ * dirs_host [n_dirs][3] and weights w_host [n_dirs] (n_dirs = n_theta*n_phi).  Synchronous. */
+fks_status fks_get_tables(const fks_ctx* h, double* a_host, double* b_host, double* dirs_host, double* w_host);
+
+/* Test-only: the per-axis whole-cell shifts delta[3][N] of the most recent transport step (host). */
+fks_status fks_get_last_shift(const fks_ctx* h, int* delta_host);
+
+/* Number of kernel launches issued by this handle since creation (instrumentation for the bench). */
+long long fks_launch_count(const fks_ctx* h);
+
+/* Synchronise `stream` and report any asynchronous CUDA error. */
+fks_status fks_sync(fks_ctx* h, void* stream);
+
+void fks_destroy(fks_ctx* h);
+const char* fks_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FKS_H */

@@ -246,11 +246,28 @@ def _along(M: np.ndarray, x: np.ndarray, axis: int) -> np.ndarray:
     return np.moveaxis(np.tensordot(M, x, axes=(1, axis)), 0, axis)
 
 
-def forward_modes(f: np.ndarray) -> np.ndarray:
+# Extended precision (x87 80-bit long double) is available for conditioning studies: near-equilibrium cells
+# have Q ~ 1e-3 of the gain/loss terms that cancel to form it.
+_PI_LD = np.longdouble("3.14159265358979323846264338327950288")
+
+
+def _cdtype(ext: bool):
+    return np.clongdouble if ext else np.complex128
+
+
+def _expmat(rows, cols, M, sign, ext):
+    """exp(sign·2πi·rows⊗cols/M) as a dense matrix (rows, cols: integer vectors)."""
+    if ext:
+        arg = np.outer(rows.astype(np.longdouble), cols.astype(np.longdouble)) * (2 * _PI_LD / np.longdouble(M))
+        return np.cos(arg) + (1j if sign > 0 else -1j) * np.sin(arg)
+    return np.exp(sign * 2j * math.pi * np.outer(rows, cols) / M)
+
+
+def forward_modes(f: np.ndarray, ext: bool = False) -> np.ndarray:
     """f̂_l = N^-3 Σ_j f_j e^{-2πi l·j/N} for l ∈ K'^3 (P:1507 discretised; A14).  f: (N, N, N) real."""
     N = f.shape[-1]
-    F = np.exp(-2j * math.pi * np.outer(kprime(N), np.arange(N)) / N)
-    x = f.astype(np.complex128)
+    F = _expmat(kprime(N), np.arange(N), N, -1, ext)
+    x = f.astype(_cdtype(ext))
     for ax in range(3):
         x = _along(F, x, ax)
     return x / N ** 3
@@ -258,7 +275,7 @@ def forward_modes(f: np.ndarray) -> np.ndarray:
 
 def inverse_modes(Qh: np.ndarray, N: int) -> np.ndarray:
     """Q_j = Σ_{k∈K'} Q̂_k e^{2πi k·j/N}, j ∈ [0,N)^3 (complex; the imaginary part is round-off, A15)."""
-    E = np.exp(2j * math.pi * np.outer(np.arange(N), kprime(N)) / N)
+    E = _expmat(np.arange(N), kprime(N), N, +1, Qh.dtype == np.clongdouble)
     x = Qh
     for ax in range(3):
         x = _along(E, x, ax)
@@ -268,7 +285,7 @@ def inverse_modes(Qh: np.ndarray, N: int) -> np.ndarray:
 def padded_inverse(Z: np.ndarray, P: int) -> np.ndarray:
     """z(p) = Σ_{l∈K'^3} Z(l) e^{2πi l·p/P}, p ∈ [0,P)^3: trig polynomial sampled on the padded grid."""
     K = kprime(Z.shape[-1] + 1)
-    E = np.exp(2j * math.pi * np.outer(np.arange(P), K) / P)
+    E = _expmat(np.arange(P), K, P, +1, Z.dtype == np.clongdouble)
     x = Z
     for ax in range(3):
         x = _along(E, x, ax)
@@ -278,8 +295,9 @@ def padded_inverse(Z: np.ndarray, P: int) -> np.ndarray:
 def padded_forward(G: np.ndarray, N: int) -> np.ndarray:
     """Ĝ_k = P^-3 Σ_p G(p) e^{-2πi k·p/P} restricted to k ∈ K'^3 (Galerkin projection)."""
     P = G.shape[-1]
-    F = np.exp(-2j * math.pi * np.outer(kprime(N), np.arange(P)) / P)
-    x = G.astype(np.complex128)
+    ext = G.dtype in (np.clongdouble, np.longdouble)
+    F = _expmat(kprime(N), np.arange(P), P, -1, ext)
+    x = G.astype(_cdtype(ext))
     for ax in range(3):
         x = _along(F, x, ax)
     return x / P ** 3
@@ -295,7 +313,7 @@ def default_pad(N: int) -> int:
 # ---------------------------------------------------------------------------------------------------
 
 def collision_fast(f: np.ndarray, tables: Tables, P: int | None = None, project_mass: bool = False,
-                   return_diag: bool = False):
+                   return_diag: bool = False, ext: bool = False):
     """Fast spectral Q for ONE cell, the paper's convolution algorithm:
 
     1. f̂ = forward_modes(f)                                               (P:1501-1510)
@@ -304,14 +322,17 @@ def collision_fast(f: np.ndarray, tables: Tables, P: int | None = None, project_
     3. Q̂_k = P^-3 Σ_p G(p) e^{-2πi k·p/P}, k ∈ K'   — exact for P ≥ 3N/2 − 2 (A10)
     4. optional (A24): Q̂_0 := 0
     5. Q_j = Σ_k Q̂_k e^{2πi k·j/N}; return Re Q (and max|Im Q| as a diagnostic, A15).
+    ext=True evaluates every step in x87 extended precision (tables stay the fp64 values), for conditioning studies.
     """
     N = f.shape[-1]
     P = P or default_pad(N)
-    fh = forward_modes(f)
-    G = np.zeros((P, P, P), dtype=np.complex128)
+    fh = forward_modes(f, ext)
+    G = np.zeros((P, P, P), dtype=_cdtype(ext))
+    a_tab = tables.a.astype(np.longdouble) if ext else tables.a
+    b_tab = tables.b.astype(np.longdouble) if ext else tables.b
     for t in range(tables.a.shape[0]):
-        A = padded_inverse(tables.a[t] * fh, P)
-        B = padded_inverse(tables.b[t] * fh, P)
+        A = padded_inverse(a_tab[t] * fh, P)
+        B = padded_inverse(b_tab[t] * fh, P)
         G += A * B
     Qh = padded_forward(G, N)
     c = N // 2 - 1
@@ -319,6 +340,8 @@ def collision_fast(f: np.ndarray, tables: Tables, P: int | None = None, project_
     if project_mass:
         Qh[c, c, c] = 0.0
     Q = inverse_modes(Qh, N)
+    if ext:
+        Q = Q.astype(np.complex128)
     if return_diag:
         return Q.real, {"max_imag": float(np.max(np.abs(Q.imag))), "Qhat0": complex(q0), "fhat": fh, "Qhat": Qh}
     return Q.real

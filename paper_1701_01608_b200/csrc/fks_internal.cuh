@@ -1,0 +1,81 @@
+// Internal declarations shared by the libfks translation units (host runtime + sm_100a kernels).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <string>
+#include <vector>
+#include "../../include/fks.h"
+
+namespace fks {
+
+constexpr int kMaxN = 64;
+
+// Per-step transport shifts passed BY VALUE as a kernel parameter (snapshotted at launch, so the host can
+// advance the generic cell for the next step immediately).  delta[a][k] = whole cells crossed along axis a
+// by velocity index k in this step (A16).
+struct Shift {
+  int nx, ny, nz, N;
+  int delta[3][kMaxN];
+};
+
+struct Ctx {
+  fks_params p{};
+  int N = 0, K = 0, P = 0, T = 0;       // K = N-1 retained modes per axis; T separated terms (+1 loss)
+  int n_theta = 0, n_phi = 0;
+  double R = 0, Rc = 0, lambda = 0;
+  int device = 0;
+  int path = FKS_PATH_AUTO;             // resolved path
+  // device tables: ab[t][l] = (a_t(l), b_t(l)), t = 0..T, l flattened over K'^3
+  double2* d_ab = nullptr;
+  std::vector<double> dirs, w;          // host copy of directions / weights
+  std::vector<double> kappa;            // exact power-of-two balance per term (device tables hold a*kappa, b/kappa)
+  // twiddles e^{+2 pi i m/M} for M = N and M = P
+  double2* d_twN = nullptr;
+  double2* d_twP = nullptr;
+  // workspace
+  void* d_ws = nullptr;
+  size_t ws_bytes = 0;
+  long long ws_cells = 0;
+  // host-buffer path staging
+  double* d_stage_in = nullptr;
+  double* d_stage_out = nullptr;
+  long long stage_cells = 0;
+  cudaStream_t stage_stream = nullptr;
+  // transport state (generic cell)
+  bool transport_ready = false;
+  int nx = 0, ny = 0, nz = 0;
+  long long cfl_num = 0, cfl_den = 1;
+  std::vector<long long> offsets;       // [3][N] in units of 1/(N*cfl_den) cell
+  Shift last{};
+  long long launches = 0;
+  int num_sms = 148;
+};
+
+// error plumbing
+void set_error(const std::string& msg);
+fks_status cuda_status(cudaError_t e, const char* what);
+
+// host quadrature (own implementation; shares nothing with the oracle)
+void gauss_legendre(int n, double a, double b, std::vector<double>& x, std::vector<double>& w);
+
+// K1 table builder (tables.cu)
+fks_status build_tables(Ctx& c);
+
+// generic path (generic.cu): Q or Euler update for n_cells cells already resident on the device.
+//   out = Q(fin)                     if euler == false
+//   out = fin + s * Q(fin)           if euler == true  (out may alias fin)
+fks_status generic_collision(Ctx& c, const double* fin, double* out, long long n_cells, bool euler, double s,
+                             cudaStream_t st);
+size_t generic_ws_bytes_per_cell(const Ctx& c);
+
+// fast path (fast32.cu)
+bool fast_available(const Ctx& c);
+fks_status fast_collision(Ctx& c, const double* fin, double* out, long long n_cells, bool euler, double s,
+                          cudaStream_t st);
+size_t fast_ws_bytes_per_cell(const Ctx& c);
+fks_status fast_prepare(Ctx& c);
+
+// transport gather (transport.cu)
+fks_status launch_transport_gather(Ctx& c, const double* fin, double* fout, const Shift& sh, cudaStream_t st);
+
+}  // namespace fks

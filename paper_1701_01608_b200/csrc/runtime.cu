@@ -1,0 +1,398 @@
+// libfks host runtime: the C ABI of include/fks.h (validation, handle, Gauss-Legendre nodes, workspace and
+// chunk planning, generic-cell transport bookkeeping).  Every compute step runs in the sm_100a kernels of
+// tables.cu / generic.cu / fast32.cu / transport.cu; there is no CPU fallback.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include "fks_internal.cuh"
+
+namespace fks {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+fks_status cuda_status(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return FKS_OK;
+  set_error(std::string(what) + ": " + cudaGetErrorString(e));
+  return e == cudaErrorMemoryAllocation ? FKS_ERR_NOMEM : FKS_ERR_CUDA;
+}
+
+// Gauss-Legendre nodes/weights on [a, b] by Newton iteration on P_n (three-term recurrence).
+void gauss_legendre(int n, double a, double b, std::vector<double>& x, std::vector<double>& w) {
+  x.assign(n, 0.0);
+  w.assign(n, 0.0);
+  const double pi = 3.14159265358979323846;
+  for (int i = 0; i < (n + 1) / 2; i++) {
+    double z = std::cos(pi * (i + 0.75) / (n + 0.5));
+    double dp = 0.0;
+    for (int it = 0; it < 100; it++) {
+      double p0 = 1.0, p1 = z;
+      for (int k = 2; k <= n; k++) {
+        double p2 = ((2.0 * k - 1.0) * z * p1 - (k - 1.0) * p0) / k;
+        p0 = p1;
+        p1 = p2;
+      }
+      if (n == 1) { p1 = z; p0 = 1.0; }
+      dp = n * (z * p1 - p0) / (z * z - 1.0);
+      double dz = p1 / dp;
+      z -= dz;
+      if (std::fabs(dz) < 1e-17) break;
+    }
+    // recompute derivative at the converged node
+    double p0 = 1.0, p1 = z;
+    for (int k = 2; k <= n; k++) {
+      double p2 = ((2.0 * k - 1.0) * z * p1 - (k - 1.0) * p0) / k;
+      p0 = p1;
+      p1 = p2;
+    }
+    if (n == 1) { p1 = z; p0 = 1.0; }
+    dp = n * (z * p1 - p0) / (z * z - 1.0);
+    double wi = 2.0 / ((1.0 - z * z) * dp * dp);
+    x[i] = -z;
+    x[n - 1 - i] = z;
+    w[i] = wi;
+    w[n - 1 - i] = wi;
+  }
+  if (n % 2 == 1) x[n / 2] = 0.0;
+  for (int i = 0; i < n; i++) {
+    x[i] = 0.5 * (b - a) * x[i] + 0.5 * (b + a);
+    w[i] = 0.5 * (b - a) * w[i];
+  }
+}
+
+static fks_status check_device_ptr(const void* p, const char* name) {
+  if (!p) { set_error(std::string(name) + " is NULL"); return FKS_ERR_INVALID; }
+  cudaPointerAttributes at;
+  cudaError_t e = cudaPointerGetAttributes(&at, p);
+  if (e != cudaSuccess) { cudaGetLastError(); set_error(std::string(name) + ": not a CUDA pointer"); return FKS_ERR_INVALID; }
+  if (at.type != cudaMemoryTypeDevice && at.type != cudaMemoryTypeManaged) {
+    set_error(std::string(name) + " must be a device pointer");
+    return FKS_ERR_INVALID;
+  }
+  return FKS_OK;
+}
+
+static bool overlap(const void* a, size_t na, const void* b, size_t nb) {
+  auto x = reinterpret_cast<uintptr_t>(a), y = reinterpret_cast<uintptr_t>(b);
+  return x < y + nb && y < x + na;
+}
+
+static fks_status sticky_check() {
+  cudaError_t e = cudaPeekAtLastError();
+  if (e != cudaSuccess) { cudaGetLastError(); return cuda_status(e, "asynchronous CUDA error"); }
+  return FKS_OK;
+}
+
+static fks_status ensure_ws(Ctx& c, size_t bytes) {
+  if (bytes <= c.ws_bytes) return FKS_OK;
+  if (c.d_ws) { cudaFree(c.d_ws); c.d_ws = nullptr; c.ws_bytes = 0; }
+  cudaError_t e = cudaMalloc(&c.d_ws, bytes);
+  if (e != cudaSuccess) { cudaGetLastError(); return cuda_status(e, "workspace allocation"); }
+  c.ws_bytes = bytes;
+  return FKS_OK;
+}
+
+static long long chunk_cells(const Ctx& c, size_t per_cell, long long n_cells) {
+  long long lim = c.p.max_cells_in_flight;
+  if (lim <= 0) {
+    size_t fr = 0, tot = 0;
+    if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) { cudaGetLastError(); fr = 8ull << 30; }
+    size_t budget = std::min<size_t>(fr / 3, 24ull << 30);
+    lim = std::max<long long>(1, (long long)(budget / std::max<size_t>(per_cell, 1)));
+  }
+  return std::min(lim, n_cells);
+}
+
+// Collision (+ optional Euler) over n cells resident on the device, chunked through the workspace.
+static fks_status run_collision(Ctx& c, const double* fin, double* out, long long n, bool euler, double s,
+                                cudaStream_t st) {
+  const bool fast = c.path == FKS_PATH_FAST;
+  size_t per_cell = fast ? fast_ws_bytes_per_cell(c) : generic_ws_bytes_per_cell(c);
+  long long ch = chunk_cells(c, per_cell, n);
+  fks_status rc = ensure_ws(c, per_cell * (size_t)ch);
+  if (rc) return rc;
+  const size_t nv = (size_t)c.N * c.N * c.N;
+  for (long long c0 = 0; c0 < n; c0 += ch) {
+    long long m = std::min(ch, n - c0);
+    rc = fast ? fast_collision(c, fin + c0 * nv, out + c0 * nv, m, euler, s, st)
+              : generic_collision(c, fin + c0 * nv, out + c0 * nv, m, euler, s, st);
+    if (rc) return rc;
+  }
+  return cuda_status(cudaPeekAtLastError(), "collision launch");
+}
+
+static Shift advance_generic_cell(Ctx& c) {
+  // Move every particle of the generic cell by v_k dt.  Units: 1/(N*cfl_den) cell; velocity
+  // index k moves (2k - N)*cfl_num units per step.  delta = floor((o + d + unit/2)/unit), o <- o + d - delta*unit,
+  // i.e. offsets stay in the half-open [-1/2, 1/2) cell (A16).
+  Shift sh{};
+  sh.nx = c.nx; sh.ny = c.ny; sh.nz = c.nz; sh.N = c.N;
+  const long long unit = (long long)c.N * c.cfl_den;
+  for (int a = 0; a < 3; a++) {
+    for (int k = 0; k < c.N; k++) {
+      long long o = c.offsets[a * c.N + k] + (2LL * k - c.N) * c.cfl_num;
+      long long num = o + unit / 2;
+      long long d = num >= 0 ? num / unit : -((-num + unit - 1) / unit);  // floor division
+      c.offsets[a * c.N + k] = o - d * unit;
+      sh.delta[a][k] = (int)d;
+    }
+  }
+  c.last = sh;
+  return sh;
+}
+
+static bool shift_is_identity(const Shift& sh) {
+  for (int a = 0; a < 3; a++) {
+    int n = a == 0 ? sh.nx : a == 1 ? sh.ny : sh.nz;
+    for (int k = 0; k < sh.N; k++)
+      if (((sh.delta[a][k] % n) + n) % n) return false;
+  }
+  return true;
+}
+
+}  // namespace fks
+
+using namespace fks;
+
+extern "C" {
+
+const char* fks_last_error(void) { return g_last_error.c_str(); }
+
+fks_status fks_collision_init(fks_ctx** out, int N, double L, int M_angles, int M_radial, int kernel) {
+  fks_params p{};
+  p.N = N; p.L = L; p.M_angles = M_angles; p.M_radial = M_radial; p.kernel = kernel;
+  return fks_collision_init_ex(out, &p);
+}
+
+fks_status fks_collision_init_ex(fks_ctx** out, const fks_params* pp) {
+  if (!out || !pp) { set_error("NULL argument"); return FKS_ERR_INVALID; }
+  *out = nullptr;
+  const fks_params& p = *pp;
+  if (p.N % 2 != 0 || p.N < 4 || p.N > kMaxN) { set_error("N must be even and in [4, 64]"); return FKS_ERR_UNSUPPORTED; }
+  if (!(p.L > 0.0) || !std::isfinite(p.L)) { set_error("L must be > 0"); return FKS_ERR_INVALID; }
+  if (p.M_angles < 1) { set_error("M_angles must be >= 1"); return FKS_ERR_INVALID; }
+  if (p.kernel != FKS_KERNEL_HARD_SPHERES && p.kernel != FKS_KERNEL_MAXWELL) { set_error("unknown kernel"); return FKS_ERR_UNSUPPORTED; }
+  if (p.kernel == FKS_KERNEL_MAXWELL && p.M_radial < 1) { set_error("M_radial must be >= 1 for Maxwell molecules"); return FKS_ERR_INVALID; }
+  if (p.quad_rule != FKS_QUAD_GL_UNIFORM && p.quad_rule != FKS_QUAD_PAPER_RECT) { set_error("unknown quadrature rule"); return FKS_ERR_UNSUPPORTED; }
+  if (p.cutoff_ratio < 0.0 || p.cutoff_ratio > (1.0 + std::sqrt(2.0)) / std::sqrt(2.0) + 1e-12) {
+    set_error("cutoff_ratio must be in [1, (1+sqrt2)/sqrt2] (A7)"); return FKS_ERR_INVALID;
+  }
+  if (p.path < FKS_PATH_AUTO || p.path > FKS_PATH_FAST) { set_error("unknown path"); return FKS_ERR_UNSUPPORTED; }
+  int P = p.pad > 0 ? p.pad : 3 * p.N / 2;
+  if (P < 3 * p.N / 2 - 2 || P > 4 * p.N) { set_error("pad must be >= 3N/2 - 2 (A10)"); return FKS_ERR_UNSUPPORTED; }
+  int nt = p.n_theta, nf = p.n_phi;
+  if (nt <= 0 || nf <= 0) {
+    nt = 1 << (int)std::ceil(std::log2((double)p.M_angles) / 2.0 - 1e-12);
+    if (p.M_angles % nt) nt = p.M_angles;
+    nf = p.M_angles / nt;
+  }
+  int nd = nt * nf;
+  int T = p.kernel == FKS_KERNEL_HARD_SPHERES ? nd : nd * p.M_radial;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) { cudaGetLastError(); return cuda_status(e, "no CUDA device"); }
+
+  Ctx* c = new (std::nothrow) Ctx();
+  if (!c) { set_error("host allocation failed"); return FKS_ERR_NOMEM; }
+  c->p = p;
+  c->N = p.N; c->K = p.N - 1; c->P = P; c->T = T;
+  c->n_theta = nt; c->n_phi = nf;
+  c->lambda = 2.0 / (3.0 + std::sqrt(2.0));
+  c->R = c->lambda * p.L;
+  c->Rc = c->R * (p.cutoff_ratio > 0.0 ? p.cutoff_ratio : 1.0);
+  c->device = dev;
+  cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, dev);
+  c->offsets.assign(3 * (size_t)p.N, 0);
+  fks_status rc = build_tables(*c);
+  if (rc) { fks_destroy(reinterpret_cast<fks_ctx*>(c)); return rc; }
+  bool fast_ok = fast_available(*c);
+  if (p.path == FKS_PATH_FAST && !fast_ok) {
+    fks_destroy(reinterpret_cast<fks_ctx*>(c));
+    set_error("fast path not instantiated for this (N, P, kernel)");
+    return FKS_ERR_UNSUPPORTED;
+  }
+  c->path = (p.path == FKS_PATH_GENERIC || !fast_ok) ? FKS_PATH_GENERIC : FKS_PATH_FAST;
+  if (c->path == FKS_PATH_FAST) {
+    rc = fast_prepare(*c);
+    if (rc) { fks_destroy(reinterpret_cast<fks_ctx*>(c)); return rc; }
+  }
+  rc = cuda_status(cudaDeviceSynchronize(), "table build");
+  if (rc) { fks_destroy(reinterpret_cast<fks_ctx*>(c)); return rc; }
+  *out = reinterpret_cast<fks_ctx*>(c);
+  return FKS_OK;
+}
+
+fks_status fks_collision_batch(fks_ctx* h, const double* f, double* Q, long long n_cells, void* stream) {
+  if (!h) { set_error("NULL handle"); return FKS_ERR_INVALID; }
+  Ctx& c = *reinterpret_cast<Ctx*>(h);
+  if (n_cells < 0) { set_error("n_cells < 0"); return FKS_ERR_INVALID; }
+  if (n_cells == 0) return FKS_OK;
+  fks_status rc;
+  if ((rc = check_device_ptr(f, "f")) || (rc = check_device_ptr(Q, "Q"))) return rc;
+  size_t bytes = (size_t)n_cells * c.N * c.N * c.N * sizeof(double);
+  if (overlap(f, bytes, Q, bytes)) { set_error("Q overlaps f"); return FKS_ERR_INVALID; }
+  if ((rc = sticky_check())) return rc;
+  return run_collision(c, f, Q, n_cells, false, 0.0, reinterpret_cast<cudaStream_t>(stream));
+}
+
+fks_status fks_transport_setup(fks_ctx* h, int nx, int ny, int nz, long long cfl_num, long long cfl_den) {
+  if (!h) { set_error("NULL handle"); return FKS_ERR_INVALID; }
+  Ctx& c = *reinterpret_cast<Ctx*>(h);
+  if (nx < 1 || ny < 1 || nz < 1) { set_error("grid dimensions must be >= 1"); return FKS_ERR_INVALID; }
+  if (cfl_den < 1 || cfl_num < 0) { set_error("cfl_den must be >= 1 and cfl_num >= 0"); return FKS_ERR_INVALID; }
+  if ((long long)nx * ny * nz > (1LL << 40)) { set_error("grid too large"); return FKS_ERR_INVALID; }
+  if ((double)c.N * (double)cfl_den * (double)(cfl_num + 1) * 4.0 > 4e18) { set_error("CFL fraction too large"); return FKS_ERR_INVALID; }
+  c.nx = nx; c.ny = ny; c.nz = nz;
+  c.cfl_num = cfl_num; c.cfl_den = cfl_den;
+  std::fill(c.offsets.begin(), c.offsets.end(), 0);
+  c.transport_ready = true;
+  return FKS_OK;
+}
+
+fks_status fks_transport_step(fks_ctx* h, const double* f_in, double* f_out, void* stream) {
+  if (!h) { set_error("NULL handle"); return FKS_ERR_INVALID; }
+  Ctx& c = *reinterpret_cast<Ctx*>(h);
+  if (!c.transport_ready) { set_error("fks_transport_setup not called"); return FKS_ERR_STATE; }
+  fks_status rc;
+  if ((rc = check_device_ptr(f_in, "f_in")) || (rc = check_device_ptr(f_out, "f_out"))) return rc;
+  long long n = (long long)c.nx * c.ny * c.nz;
+  size_t bytes = (size_t)n * c.N * c.N * c.N * sizeof(double);
+  if (overlap(f_in, bytes, f_out, bytes)) { set_error("f_out overlaps f_in"); return FKS_ERR_INVALID; }
+  if ((rc = sticky_check())) return rc;
+  Shift sh = advance_generic_cell(c);
+  return launch_transport_gather(c, f_in, f_out, sh, reinterpret_cast<cudaStream_t>(stream));
+}
+
+fks_status fks_step(fks_ctx* h, const double* f_in, double* f_out, double coll_scale, void* stream) {
+  if (!h) { set_error("NULL handle"); return FKS_ERR_INVALID; }
+  Ctx& c = *reinterpret_cast<Ctx*>(h);
+  if (!c.transport_ready) { set_error("fks_transport_setup not called"); return FKS_ERR_STATE; }
+  if (!std::isfinite(coll_scale)) { set_error("coll_scale must be finite"); return FKS_ERR_INVALID; }
+  fks_status rc;
+  if ((rc = check_device_ptr(f_in, "f_in")) || (rc = check_device_ptr(f_out, "f_out"))) return rc;
+  long long n = (long long)c.nx * c.ny * c.nz;
+  size_t bytes = (size_t)n * c.N * c.N * c.N * sizeof(double);
+  if (overlap(f_in, bytes, f_out, bytes)) { set_error("f_out overlaps f_in"); return FKS_ERR_INVALID; }
+  if ((rc = sticky_check())) return rc;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  Shift sh = advance_generic_cell(c);
+  if (shift_is_identity(sh)) return run_collision(c, f_in, f_out, n, true, coll_scale, st);
+  // transport (exact permutation) into f_out, then collision + Euler in place on f_out
+  rc = launch_transport_gather(c, f_in, f_out, sh, st);
+  if (rc) return rc;
+  return run_collision(c, f_out, f_out, n, true, coll_scale, st);
+}
+
+static fks_status ensure_stage(Ctx& c, long long cells) {
+  if (cells <= c.stage_cells) return FKS_OK;
+  if (c.d_stage_in) cudaFree(c.d_stage_in);
+  if (c.d_stage_out) cudaFree(c.d_stage_out);
+  c.d_stage_in = c.d_stage_out = nullptr;
+  c.stage_cells = 0;
+  size_t bytes = (size_t)cells * c.N * c.N * c.N * sizeof(double);
+  cudaError_t e = cudaMalloc(&c.d_stage_in, bytes);
+  if (e == cudaSuccess) e = cudaMalloc(&c.d_stage_out, bytes);
+  if (e != cudaSuccess) { cudaGetLastError(); return cuda_status(e, "staging allocation"); }
+  if (!c.stage_stream) cudaStreamCreateWithFlags(&c.stage_stream, cudaStreamNonBlocking);
+  c.stage_cells = cells;
+  return FKS_OK;
+}
+
+fks_status fks_collision_batch_host(fks_ctx* h, const double* f_host, double* Q_host, long long n_cells) {
+  if (!h) { set_error("NULL handle"); return FKS_ERR_INVALID; }
+  Ctx& c = *reinterpret_cast<Ctx*>(h);
+  if (n_cells < 0 || (n_cells > 0 && (!f_host || !Q_host))) { set_error("bad host buffers"); return FKS_ERR_INVALID; }
+  if (n_cells == 0) return FKS_OK;
+  fks_status rc;
+  if ((rc = sticky_check())) return rc;
+  if ((rc = ensure_stage(c, n_cells))) return rc;
+  const size_t bytes = (size_t)n_cells * c.N * c.N * c.N * sizeof(double);
+  cudaStream_t st = c.stage_stream;
+  if ((rc = cuda_status(cudaMemcpyAsync(c.d_stage_in, f_host, bytes, cudaMemcpyHostToDevice, st), "H2D"))) return rc;
+  if ((rc = run_collision(c, c.d_stage_in, c.d_stage_out, n_cells, false, 0.0, st))) return rc;
+  if ((rc = cuda_status(cudaMemcpyAsync(Q_host, c.d_stage_out, bytes, cudaMemcpyDeviceToHost, st), "D2H"))) return rc;
+  return cuda_status(cudaStreamSynchronize(st), "host-buffer collision");
+}
+
+fks_status fks_step_host(fks_ctx* h, const double* f_in_host, double* f_out_host, double coll_scale) {
+  if (!h) { set_error("NULL handle"); return FKS_ERR_INVALID; }
+  Ctx& c = *reinterpret_cast<Ctx*>(h);
+  if (!c.transport_ready) { set_error("fks_transport_setup not called"); return FKS_ERR_STATE; }
+  if (!f_in_host || !f_out_host) { set_error("bad host buffers"); return FKS_ERR_INVALID; }
+  long long n = (long long)c.nx * c.ny * c.nz;
+  fks_status rc;
+  if ((rc = sticky_check())) return rc;
+  if ((rc = ensure_stage(c, n))) return rc;
+  const size_t bytes = (size_t)n * c.N * c.N * c.N * sizeof(double);
+  cudaStream_t st = c.stage_stream;
+  if ((rc = cuda_status(cudaMemcpyAsync(c.d_stage_in, f_in_host, bytes, cudaMemcpyHostToDevice, st), "H2D"))) return rc;
+  if ((rc = fks_step(h, c.d_stage_in, c.d_stage_out, coll_scale, st))) return rc;
+  if ((rc = cuda_status(cudaMemcpyAsync(f_out_host, c.d_stage_out, bytes, cudaMemcpyDeviceToHost, st), "D2H"))) return rc;
+  return cuda_status(cudaStreamSynchronize(st), "host-buffer step");
+}
+
+fks_status fks_get_info(const fks_ctx* h, int* P, int* T, double* R, double* lambda) {
+  if (!h) { set_error("NULL handle"); return FKS_ERR_INVALID; }
+  const Ctx& c = *reinterpret_cast<const Ctx*>(h);
+  if (P) *P = c.P;
+  if (T) *T = c.T;
+  if (R) *R = c.Rc;
+  if (lambda) *lambda = c.lambda;
+  return FKS_OK;
+}
+
+fks_status fks_get_tables(const fks_ctx* h, double* a_host, double* b_host, double* dirs_host, double* w_host) {
+  if (!h) { set_error("NULL handle"); return FKS_ERR_INVALID; }
+  const Ctx& c = *reinterpret_cast<const Ctx*>(h);
+  size_t nl = (size_t)c.K * c.K * c.K, n = (size_t)(c.T + 1) * nl;
+  if (a_host || b_host) {
+    std::vector<double2> tmp(n);
+    fks_status rc = cuda_status(cudaMemcpy(tmp.data(), c.d_ab, n * sizeof(double2), cudaMemcpyDeviceToHost), "table copy");
+    if (rc) return rc;
+    for (size_t i = 0; i < n; i++) {
+      const double k = c.kappa.empty() ? 1.0 : c.kappa[i / nl];  // undo the exact power-of-two balancing
+      if (a_host) a_host[i] = tmp[i].x / k;
+      if (b_host) b_host[i] = tmp[i].y * k;
+    }
+  }
+  if (dirs_host) std::memcpy(dirs_host, c.dirs.data(), c.dirs.size() * sizeof(double));
+  if (w_host) std::memcpy(w_host, c.w.data(), c.w.size() * sizeof(double));
+  return FKS_OK;
+}
+
+fks_status fks_get_last_shift(const fks_ctx* h, int* delta_host) {
+  if (!h || !delta_host) { set_error("NULL argument"); return FKS_ERR_INVALID; }
+  const Ctx& c = *reinterpret_cast<const Ctx*>(h);
+  for (int a = 0; a < 3; a++)
+    for (int k = 0; k < c.N; k++) delta_host[a * c.N + k] = c.last.delta[a][k];
+  return FKS_OK;
+}
+
+long long fks_launch_count(const fks_ctx* h) {
+  return h ? reinterpret_cast<const Ctx*>(h)->launches : -1;
+}
+
+fks_status fks_sync(fks_ctx* h, void* stream) {
+  (void)h;
+  fks_status rc = cuda_status(cudaStreamSynchronize(reinterpret_cast<cudaStream_t>(stream)), "stream sync");
+  if (rc) return rc;
+  return sticky_check();
+}
+
+void fks_destroy(fks_ctx* h) {
+  if (!h) return;
+  Ctx* c = reinterpret_cast<Ctx*>(h);
+  if (c->d_ab) cudaFree(c->d_ab);
+  if (c->d_twN) cudaFree(c->d_twN);
+  if (c->d_twP) cudaFree(c->d_twP);
+  if (c->d_ws) cudaFree(c->d_ws);
+  if (c->d_stage_in) cudaFree(c->d_stage_in);
+  if (c->d_stage_out) cudaFree(c->d_stage_out);
+  if (c->stage_stream) cudaStreamDestroy(c->stage_stream);
+  delete c;
+}
+
+}  // extern "C"

@@ -1,0 +1,74 @@
+"""CPU checks of the boundary: libfks.so builds for sm_100a, loads, and exports every symbol fks.h declares;
+without a GPU every compute entry fails loudly (there is no CPU fallback)."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+from paper_1701_01608_b200 import binding, build
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    build.build()
+    return binding.load_library()
+
+
+def header_symbols():
+    src = open(os.path.join(ROOT, "include", "fks.h")).read()
+    return sorted(set(re.findall(r"\b(fks_[a-z_]+)\s*\(", src)))
+
+
+def test_header_and_binding_agree():
+    assert header_symbols() == sorted(binding.EXPORTS)
+
+
+def test_library_exports_every_symbol(lib):
+    for name in header_symbols():
+        assert hasattr(lib, name), name
+    out = subprocess.run(["nm", "-D", "--defined-only", build.LIB], capture_output=True, text=True).stdout
+    for name in header_symbols():
+        assert re.search(rf"\bT {name}\b", out), name
+
+
+def test_sm100a_code_present(lib):
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", build.LIB], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_fails_loudly_without_gpu(lib):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    h = ctypes.c_void_p()
+    st = lib.fks_collision_init(ctypes.byref(h), 16, 13.24, 16, 16, 0)
+    assert st == binding.FKS_ERR_CUDA and h.value is None
+    assert lib.fks_last_error()
+    with pytest.raises(binding.FksError):
+        binding.Collision(16, 13.24)
+
+
+def test_argument_validation_without_gpu(lib):
+    h = ctypes.c_void_p()
+    assert lib.fks_collision_init(ctypes.byref(h), 15, 13.24, 16, 16, 0) == binding.FKS_ERR_UNSUPPORTED
+    assert lib.fks_collision_init(ctypes.byref(h), 130, 13.24, 16, 16, 0) == binding.FKS_ERR_UNSUPPORTED
+    assert lib.fks_collision_init(ctypes.byref(h), 16, -1.0, 16, 16, 0) == binding.FKS_ERR_INVALID
+    assert lib.fks_collision_init(ctypes.byref(h), 16, 13.24, 0, 16, 0) == binding.FKS_ERR_INVALID
+    assert lib.fks_collision_init(ctypes.byref(h), 16, 13.24, 16, 0, 1) == binding.FKS_ERR_INVALID
+    assert lib.fks_collision_init(ctypes.byref(h), 16, 13.24, 16, 16, 7) == binding.FKS_ERR_UNSUPPORTED
+    assert lib.fks_collision_batch(None, None, None, 1, None) == binding.FKS_ERR_INVALID
+    assert lib.fks_step(None, None, None, 0.1, None) == binding.FKS_ERR_INVALID
+
+
+def test_product_never_imports_oracle():
+    pkg = os.path.join(ROOT, "paper_1701_01608_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for fn in files:
+            if fn.endswith((".py", ".cu", ".cuh", ".cpp", ".h")):
+                txt = open(os.path.join(dirpath, fn)).read()
+                assert not re.search(r"^\s*(from|import)\s+oracle", txt, re.M), fn
+                assert "fks_oracle" not in txt, fn

@@ -1,0 +1,212 @@
+"""GPU parity: libfks (through the C ABI) vs the CPU oracle on the same seeded inputs.
+
+Tolerances: tables ≤ 1e-13·max|table| (P17); Q per cell ≤ 1e-10 relative L∞ (BJ.north_star, A23);
+transport bit-exact (A25); mass defect |ΣQ|/Σ|Q_loss| ≤ 1e-11 (A24).
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import fks_oracle as o
+from paper_1701_01608_b200 import binding as B
+from paper_1701_01608_b200 import inputs
+from paper_1701_01608_b200.configs import CONFIGS, L_BOX
+from tests._common import TOL_Q, TOL_TABLE, cfg_tables, oracle_tables, oracle_Q, rel_err_per_cell
+
+pytestmark = pytest.mark.gpu
+
+
+def make(cfg, path=B.FKS_PATH_AUTO, **kw):
+    return B.Collision(cfg.N, cfg.L, cfg.M, cfg.M_r, cfg.kernel, path=path, **kw)
+
+
+# ---------------- P17: tables -------------------------------------------------------------------------
+
+@pytest.mark.parametrize("name", ["c0", "c1", "c2", "c4"])
+def test_tables_match_oracle(cuda_device, name):
+    cfg = CONFIGS[name]
+    col = make(cfg)
+    ref = cfg_tables(name)
+    e, w = o.directions(*o.split_angles(cfg.M))
+    a, b, dirs, ww = B.fks_get_tables(col.h, cfg.N, len(w))
+    assert np.abs(dirs - e).max() < 1e-15 and np.abs(ww - w).max() < 1e-15
+    assert a.shape == ref.a.shape
+    assert np.abs(a - ref.a).max() <= TOL_TABLE * np.abs(ref.a).max()
+    assert np.abs(b - ref.b).max() <= TOL_TABLE * np.abs(ref.b).max()
+
+
+@pytest.mark.parametrize("kw", [dict(quad_rule=1), dict(cutoff_ratio=1.5), dict(n_theta=2, n_phi=3)])
+def test_tables_variants(cuda_device, kw):
+    col = B.Collision(12, L_BOX, 16, 16, 0, **kw)
+    ref = oracle_tables(12, L_BOX, 16, 16, 0, n_theta=kw.get("n_theta", 0), n_phi=kw.get("n_phi", 0),
+                        rule=kw.get("quad_rule", 0), cutoff_ratio=kw.get("cutoff_ratio", 1.0))
+    nd = ref.w.size
+    a, b, _, _ = B.fks_get_tables(col.h, 12, nd)
+    assert np.abs(a - ref.a).max() <= TOL_TABLE * np.abs(ref.a).max()
+    assert np.abs(b - ref.b).max() <= TOL_TABLE * np.abs(ref.b).max()
+
+
+# ---------------- collision: small configs in full ----------------------------------------------------
+
+@pytest.mark.parametrize("name", ["c0", "c1"])
+def test_collision_config_full(cuda_device, name):
+    cfg = CONFIGS[name]
+    f = inputs.make_f(cfg, device=cuda_device)
+    col = make(cfg)
+    Q = col.collision_batch(f)
+    torch.cuda.synchronize()
+    fh, qh = f.cpu().numpy(), Q.cpu().numpy()
+    tb = cfg_tables(name)
+    ref = oracle_Q(fh, tb)
+    err = rel_err_per_cell(qh, ref)
+    assert err.max() <= TOL_Q, err.max()
+    loss = np.stack([np.abs(o.loss_part(x, tb)).sum() for x in fh])
+    assert (np.abs(qh.reshape(len(fh), -1).sum(1)) / loss).max() <= 1e-11
+
+
+@pytest.mark.parametrize("N", [4, 6, 8, 12, 16])
+@pytest.mark.parametrize("kernel", [0, 1])
+def test_collision_random_fields_vs_direct_sum(cuda_device, N, kernel):
+    M_r = 4
+    f = inputs.random_field(3, N, seed=N + 10 * kernel, signed=(N % 4 == 0)).to(cuda_device)
+    col = B.Collision(N, L_BOX, 16, M_r, kernel)
+    Q = col.collision_batch(f).cpu().numpy()
+    tb = oracle_tables(N, L_BOX, 16, M_r, kernel)
+    ref = np.stack([o.collision_direct(x, tb) for x in f.cpu().numpy()])
+    assert rel_err_per_cell(Q, ref).max() <= TOL_Q
+
+
+@pytest.mark.parametrize("pad", [0, 22, 32])
+def test_collision_pad_and_projection(cuda_device, pad):
+    N = 16
+    cfg = CONFIGS["c0"]
+    f = inputs.make_f(cfg, device=cuda_device)[:3]
+    col = B.Collision(N, L_BOX, 16, 16, 0, pad=pad, project_mass=1)
+    Q = col.collision_batch(f).cpu().numpy()
+    ref = oracle_Q(f.cpu().numpy(), cfg_tables("c0"), P=pad or None, project_mass=True)
+    assert rel_err_per_cell(Q, ref).max() <= TOL_Q
+    assert np.abs(Q.reshape(3, -1).sum(1)).max() <= 1e-13 * np.abs(Q).max() * Q[0].size
+
+
+def test_collision_bkw_report(cuda_device):
+    """c1 (BKW, N = 24): Q vs the analytic ∂f/∂t.  Resolution-limited (~0.2-0.5, P14): reported,
+    gated only loosely; the 1e-6 BKW pin is the oracle's N = 64 test."""
+    cfg = CONFIGS["c1"]
+    f = inputs.make_f(cfg, device=cuda_device)[:4]
+    Q = make(cfg).collision_batch(f).cpu().numpy()
+    Ks = inputs.cell_params(cfg)[:4, 0, 0]
+    v3 = o.velocity_grid3(cfg.N, cfg.L)
+    for q, K in zip(Q, Ks):
+        ex = o.bkw_dfdt(v3, K)
+        assert np.abs(q - ex).max() / np.abs(ex).max() < 1.0
+
+
+# ---------------- edge cases ---------------------------------------------------------------------------
+
+def test_edge_cases(cuda_device):
+    col = B.Collision(8, L_BOX, 16, 16, 0)
+    f = torch.rand(4, 8, 8, 8, dtype=torch.float64, device=cuda_device)
+    Q = torch.full_like(f, 7.0)
+    B.fks_collision_batch(col.h, f, Q, 0)                      # n_cells = 0: no-op
+    torch.cuda.synchronize()
+    assert (Q == 7.0).all()
+    with pytest.raises(B.FksError) as ei:
+        B.fks_collision_batch(col.h, f, f, 4)                   # overlap
+    assert ei.value.status == B.FKS_ERR_INVALID
+    with pytest.raises(B.FksError) as ei:
+        B.fks_collision_batch(col.h, f.cpu(), Q, 4)             # host pointer
+    assert ei.value.status == B.FKS_ERR_INVALID
+    with pytest.raises(B.FksError) as ei:
+        B.fks_step(col.h, f, Q, 0.1)                            # before transport setup
+    assert ei.value.status == B.FKS_ERR_STATE
+    # one cell, ragged counts
+    for n in (1, 3):
+        Q = col.collision_batch(f[:n].contiguous())
+        ref = oracle_Q(f[:n].cpu().numpy(), oracle_tables(8, L_BOX, 16, 16, 0))
+        assert rel_err_per_cell(Q.cpu().numpy(), ref).max() <= TOL_Q
+    B.fks_sync(col.h)
+
+
+def test_chunking_matches_unchunked(cuda_device):
+    cfg = CONFIGS["c0"]
+    f = inputs.make_f(cfg, device=cuda_device)
+    q1 = B.Collision(16, L_BOX, 16, 16, 0).collision_batch(f)
+    q2 = B.Collision(16, L_BOX, 16, 16, 0, max_cells_in_flight=3).collision_batch(f)
+    assert torch.equal(q1, q2)
+
+
+# ---------------- transport and the step ---------------------------------------------------------------
+
+def test_transport_bit_exact(cuda_device):
+    N, shape = 8, (5, 4, 3)
+    n = 60
+    f = torch.rand(n, N, N, N, dtype=torch.float64, device=cuda_device)
+    col = B.Collision(N, L_BOX, 16, 16, 0)
+    col.transport_setup(shape, 7, 3)
+    cell = o.GenericCell(N=N, c_num=7, c_den=3)
+    ref = f.cpu().numpy()
+    cur = f
+    for _ in range(4):
+        out = torch.empty_like(cur)
+        col.transport_step(cur, out)
+        d = cell.advance()
+        assert np.array_equal(col.last_shift(), d)
+        ref = o.transport(ref, shape, d)
+        assert np.array_equal(out.cpu().numpy(), ref)
+        cur = out
+
+
+def test_step_homogeneous_c0(cuda_device):
+    cfg = CONFIGS["c0"]
+    f = inputs.make_f(cfg, device=cuda_device)
+    col = make(cfg)
+    col.transport_setup(cfg.shape, 0, 1)
+    out = torch.empty_like(f)
+    s = cfg.coll_scale
+    col.step(f, out, s)
+    fh = f.cpu().numpy()
+    Q = oracle_Q(fh, cfg_tables("c0"))
+    got = out.cpu().numpy()
+    dq = (got - fh) / s
+    assert rel_err_per_cell(dq, Q).max() <= 1e-9
+    assert np.abs(got.sum() - fh.sum()) / np.abs(fh).sum() <= 1e-12      # mass per step (A24)
+
+
+def test_step_with_transport(cuda_device):
+    N, shape = 16, (4, 3, 2)
+    cfg = CONFIGS["c0"]
+    n = 24
+    f = inputs.random_field(n, N, seed=3).to(cuda_device) * 0.01 + inputs.make_f(cfg, device=cuda_device)[:1]
+    col = B.Collision(N, L_BOX, 16, 16, 0)
+    col.transport_setup(shape, 1, 2)
+    cell = o.GenericCell(N=N, c_num=1, c_den=2)
+    tb = cfg_tables("c0")
+    cur = f
+    ref = f.cpu().numpy()
+    s = 0.01
+    for _ in range(2):
+        out = torch.empty_like(cur)
+        col.step(cur, out, s)
+        ref = o.fks_step(ref, shape, cell, tb, s)
+        got = out.cpu().numpy()
+        dq_ref = ref - o.transport(cur.cpu().numpy(), shape, col.last_shift())
+        dq = got - o.transport(cur.cpu().numpy(), shape, col.last_shift())
+        assert rel_err_per_cell(dq, dq_ref).max() <= 1e-9
+        cur = out
+        ref = got  # continue from the GPU state so both see identical inputs
+
+
+# ---------------- full-size configs on sampled cells ------------------------------------------------------
+
+@pytest.mark.parametrize("name", ["c2", "c3"])
+def test_collision_config_sampled(cuda_device, name):
+    cfg = CONFIGS[name]
+    f = inputs.make_f(cfg, device=cuda_device)
+    col = make(cfg)
+    Q = col.collision_batch(f)
+    torch.cuda.synchronize()
+    cells = inputs.sample_cells(cfg, 4)
+    fh = f[cells].cpu().numpy()
+    ref = oracle_Q(fh, cfg_tables(name))
+    assert rel_err_per_cell(Q[cells].cpu().numpy(), ref).max() <= TOL_Q
+    del f, Q

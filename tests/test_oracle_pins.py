@@ -363,3 +363,19 @@ def test_P16_euler(hs16):
     g1 = o.fks_step(f, (1, 1, 1), cell, hs16, 0.01)
     g2 = o.fks_step(f, (1, 1, 1), cell, hs16, 0.02)
     assert np.abs((g2 - f) - 2 * (g1 - f)).max() < 1e-15 and np.abs(g1[0] - f[0] - 0.01 * Q).max() < 1e-16
+
+
+# ---------------- conditioning: fp64 oracle vs the same steps in extended precision ----------------------
+
+def test_fp64_oracle_vs_extended_precision():
+    """Near-equilibrium cells (c2/c3-like) have ‖Q‖ ~ 5e-4·‖Q_loss‖: the fp64 oracle must still agree with an
+    x87 extended-precision evaluation of the same steps to ≤ 1e-10 relative (measured ~5e-12)."""
+    N = 32
+    tb = o.build_tables(N, L, M=32)
+    v3 = o.velocity_grid3(N, L)
+    f = o.maxwellian(v3, 1.0, (1e-3, -5e-4, 2e-4), 1.0)
+    f[np.linalg.norm(v3, axis=-1) > R] = 0
+    q64 = o.collision_fast(f, tb)
+    qx = o.collision_fast(f, tb, ext=True)
+    assert np.abs(q64 - qx).max() <= 1e-10 * np.abs(qx).max()
+    assert np.abs(q64 - qx).max() <= 1e-14 * np.abs(o.loss_part(f, tb)).max()
