@@ -1,0 +1,310 @@
+#!/usr/bin/env python
+"""Benchmark of the FKS hot path on B200.
+
+One "step" = one fks_step over the whole workload: exact transport gather (a1) + forward transform (a2) +
+T+1 separated terms (a3-a5) + back transform and explicit Euler write-back (a6-a7) + generic-cell
+bookkeeping (a8).  Default workload: BASELINE.json configs[3] (c3: 32^3 cells x 32^3 velocities, hard
+spheres, M = 32), the configuration the headline target is quoted on.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl ours|reference]
+
+N > 1 is launched by torchrun: every rank runs its own c3 box (independent cells, no data-path collective:
+weak scaling); time = max over ranks of the CUDA-event time; rank 0 prints ONE JSON line.
+`--impl reference` times the CPU oracle (tests' reference implementation) on a bounded sample of the same
+workload, on rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+MEASURED_PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FP64_UNITS_PER_SM = 64          # DFMA lanes per SM per clock (B200, sm_100a)
+N_SMS = 148
+
+
+def flops_per_cell(N: int, P: int, T: int) -> dict:
+    """Algorithmic FLOPs per cell: conventional FFT counts (5 n log2 n per
+    complex length-n transform, 2.5 for real) of the pruned Galerkin computation + element-wise work."""
+    K = N - 1
+    lg = math.log2
+    fwd = 2.5 * N ** 3 * lg(N ** 3)
+    inv_term = 5 * P * lg(P) * (K * K + K * P + P * P)
+    elem_term = 4 * K ** 3 + 2 * P ** 3
+    back = 2.5 * P * lg(P) * (P * P + P * K + K * K) + 2.5 * N ** 3 * lg(N ** 3)
+    hot = (T + 1) * (inv_term + elem_term)
+    return {"forward": fwd, "hot": hot, "back": back, "total": fwd + hot + back}
+
+
+def fp64_peak_tflops(sm_mhz: float) -> float:
+    return N_SMS * FP64_UNITS_PER_SM * 2 * sm_mhz * 1e6 / 1e12
+
+
+# ------------------------------------------------------------------------------------------------------
+# clocks during the timed region
+# ------------------------------------------------------------------------------------------------------
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_bench_{os.getpid()}.csv")
+
+    def __enter__(self):
+        try:
+            os.makedirs(os.path.dirname(self.path), exist_ok=True)
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=self.fh, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.fh.close()
+
+    def summary(self) -> dict:
+        rows = []
+        try:
+            for line in open(self.path):
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) >= 8:
+                    rows.append(parts)
+        except Exception:
+            pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = sorted(float(r[0]) for r in rows if r[0].replace(".", "").isdigit())
+        mx = max(float(r[1]) for r in rows if r[1].replace(".", "").isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i] == "Active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(rows), "power_w_max": max(float(r[2]) for r in rows)}
+
+
+# ------------------------------------------------------------------------------------------------------
+# CPU oracle timing (cpu_baseline / --impl reference)
+# ------------------------------------------------------------------------------------------------------
+
+def oracle_threads() -> int:
+    try:
+        from threadpoolctl import threadpool_info
+        n = [i.get("num_threads", 1) for i in threadpool_info() if i.get("user_api") == "blas"]
+        return max(n) if n else 1
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def time_oracle(cfg, budget_s: float, max_cells: int = 256) -> dict:
+    """Oracle fks_step on sampled cells of the workload (transport is a permutation of inputs; collision +
+    Euler per sampled cell), until `budget_s` of CPU time has elapsed."""
+    import numpy as np
+    from oracle import fks_oracle as o
+    from paper_1701_01608_b200 import inputs
+    tb = o.build_tables(cfg.N, cfg.L, M=cfg.M, M_r=cfg.M_r, kernel=cfg.kernel)
+    cells = inputs.sample_cells(cfg, min(max_cells, cfg.n_cells), seed=5)
+    f = inputs.make_f(cfg, cells=cells).numpy()
+    t0 = time.perf_counter()
+    n = 0
+    for fc in f:
+        o.euler(fc, o.collision_fast(fc, tb), cfg.coll_scale)
+        n += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    dt = time.perf_counter() - t0
+    return {"cells": n, "seconds": dt, "value": n * cfg.N ** 3 / dt}
+
+
+# ------------------------------------------------------------------------------------------------------
+
+def dist_info():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c3")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+
+    from paper_1701_01608_b200.configs import CONFIGS
+    cfg = CONFIGS[args.config]
+    ws, rank, local = dist_info()
+    metric = "fp64 Q(f,f) cell·velocity-points/s on 1 B200; fraction of FP64/HBM roofline"
+    unit = "cell·vp/s"
+    workload = {"workload": f"{cfg.name}: {cfg.shape[0]}x{cfg.shape[1]}x{cfg.shape[2]} cells x {cfg.N}^3 velocities, "
+                            f"{'hard spheres' if cfg.kernel == 0 else 'Maxwell molecules'}, M={cfg.M}, fks_step "
+                            f"(transport c={cfg.cfl_num}/{cfg.cfl_den} + collision + Euler, s={cfg.coll_scale:.6g})",
+                "config": cfg.name, "n_cells": cfg.n_cells, "N": cfg.N, "M": cfg.M,
+                "l2": "inputs larger than L2 (f is %.2f GB per copy)" % (cfg.n_cells * cfg.N ** 3 * 8 / 1e9)}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        times = []
+        cells = 0
+        per_step = max(2.0, min(args.cpu_seconds, 120.0 / max(1, args.steps + args.warmup)))
+        for i in range(args.warmup + args.steps):
+            r = time_oracle(cfg, per_step, max_cells=8)
+            if i >= args.warmup:
+                times.append(r["seconds"])
+                cells += r["cells"]
+        val = cells * cfg.N ** 3 / sum(times)
+        line = {"impl": "reference", "metric": metric, "value": val, "unit": unit, "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic", "config": workload,
+                "cpu_baseline": {"value": val, "unit": unit, "cores": oracle_threads(), "kind": "oracle",
+                                 "sample": f"{cells} cells of {cfg.name} (collision+Euler per sampled cell), "
+                                           f"{args.steps} steps of ~{per_step:.0f} s"},
+                "e2e": {"value": val, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_1701_01608_b200 import binding as B
+    from paper_1701_01608_b200 import inputs
+
+    if ws > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", init_method="env://")
+    dev = torch.device("cuda", local if ws > 1 else 0)
+    torch.cuda.set_device(dev)
+    stream = torch.cuda.current_stream(dev)
+
+    col = B.Collision(cfg.N, cfg.L, cfg.M, cfg.M_r, cfg.kernel)
+    P, T = col.info["P"], col.info["T"]
+    fa = inputs.make_f(cfg, device=dev, seed=None if rank == 0 else rank)
+    fb = torch.empty_like(fa)
+    col.transport_setup(cfg.shape, cfg.cfl_num, cfg.cfl_den)
+    s = cfg.coll_scale
+
+    def barrier():
+        if ws > 1:
+            dist.barrier()
+
+    bufs = [fa, fb]
+    for i in range(args.warmup):
+        col.step(bufs[i % 2], bufs[(i + 1) % 2], s)
+    torch.cuda.synchronize()
+    barrier()
+    B.fks_profile(col.h, True)
+    B.fks_profile_read(col.h)  # reset
+    n0 = col.launches()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev.index or 0) as clk:
+        torch.cuda.synchronize()
+        barrier()
+        e0.record(stream)
+        for i in range(args.steps):
+            col.step(bufs[(args.warmup + i) % 2], bufs[(args.warmup + i + 1) % 2], s)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    ms_total = e0.elapsed_time(e1)
+    launches = col.launches() - n0
+    ph_ms, ph_cnt = B.fks_profile_read(col.h)
+    B.fks_profile(col.h, False)
+    if ws > 1:
+        t = torch.tensor([ms_total], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+    ms_step = ms_total / args.steps
+    cells_all = cfg.n_cells * ws
+    value = cells_all * cfg.N ** 3 / (ms_step / 1e3)
+
+    # roofline of the dominant kernel (the term loop / hot kernel, phase 2)
+    fl = flops_per_cell(cfg.N, P, T)
+    hot_ms = ph_ms[2] / max(1, ph_cnt[2])
+    cells_per_launch = cfg.n_cells * args.steps / max(1, ph_cnt[2])
+    achieved = fl["hot"] * cells_per_launch / (hot_ms / 1e3) / 1e12
+    peak = fp64_peak_tflops(1965.0)
+    clocks = clk.summary()
+
+    # end to end through the host-buffer C-ABI call (pinned host memory, copies inside the timed region)
+    e2e = None
+    if not args.no_e2e:
+        hin = torch.empty(fa.shape, dtype=torch.float64, pin_memory=True)
+        hout = torch.empty_like(hin, pin_memory=True)
+        hin.copy_(fa)
+        col.transport_setup(cfg.shape, cfg.cfl_num, cfg.cfl_den)
+        B.fks_step_host(col.h, hin, hout, s)  # warm-up (allocates staging)
+        barrier()
+        t0 = time.perf_counter()
+        for i in range(args.e2e_steps):
+            B.fks_step_host(col.h, hin if i % 2 == 0 else hout, hout if i % 2 == 0 else hin, s)
+        dt = time.perf_counter() - t0
+        if ws > 1:
+            t = torch.tensor([dt], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
+        nbytes = cfg.n_cells * cfg.N ** 3 * 8
+        e2e = {"value": cells_all * cfg.N ** 3 * args.e2e_steps / dt, "unit": unit,
+               "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes, "steps": args.e2e_steps,
+               "api": "fks_step_host (pinned host buffers)"}
+        del hin, hout
+
+    if rank != 0:
+        if ws > 1:
+            dist.destroy_process_group()
+        return
+
+    cpu = time_oracle(cfg, args.cpu_seconds)
+    line = {
+        "metric": metric, "value": value, "unit": unit, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": workload,
+        "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak, "traffic": None,
+                     "kernel": "term loop (a3-a5: table product, pruned 3D inverse, gain-loss accumulate)",
+                     "flop_per_cell": fl["hot"], "cells_per_launch": cells_per_launch, "ms_per_launch": hot_ms,
+                     "peak_note": "FP64 DFMA: 148 SM x 64 lanes x 2 flop x 1965 MHz (unit counts, max clock); "
+                                  "measured DFMA microbench 33.6 TF/s (profiles/r01_box_microbench.jsonl)"},
+        "whole_step": {"flop_per_cell": fl["total"],
+                       "tflops": fl["total"] * cells_all / ws / (ms_step / 1e3) / 1e12,
+                       "frac_of_fp64_peak": fl["total"] * cells_all / ws / (ms_step / 1e3) / 1e12 / peak,
+                       "hbm_bytes_per_cell": 16 * cfg.N ** 3},
+        "phases_ms_per_step": {"transport": ph_ms[0] / args.steps, "forward": ph_ms[1] / args.steps,
+                               "term_loop": ph_ms[2] / args.steps, "back": ph_ms[3] / args.steps},
+        "path": {1: "generic", 2: "fast"}.get(col.info.get("path"), None),
+        "clocks": clocks, "gpu_launches": launches, "e2e": e2e,
+        "cpu_baseline": {"value": cpu["value"], "unit": unit, "cores": oracle_threads(), "kind": "oracle",
+                         "sample": f"{cpu['cells']} sampled cells of {cfg.name}, collision+Euler, "
+                                   f"{cpu['seconds']:.1f} s (numpy fp64 oracle, naive DFT matrices)"},
+    }
+    print(json.dumps(line))
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -106,12 +106,23 @@ fks_status fks_step_host(fks_ctx* h, const double* f_in_host, double* f_out_host
  * lambda = 2/(3+sqrt 2).  Any out pointer may be NULL. */
 fks_status fks_get_info(const fks_ctx* h, int* P, int* T, double* R, double* lambda);
 
+/* The path this handle runs (fks_path: FKS_PATH_GENERIC or FKS_PATH_FAST); -1 for a NULL handle. */
+int fks_get_path(const fks_ctx* h);
+
 /* Test-only: copy the tables to host arrays a_host, b_host [(T+1)][N-1][N-1][N-1], the directions
  * dirs_host [n_dirs][3] and weights w_host [n_dirs] (n_dirs = n_theta*n_phi).  Synchronous. */
 fks_status fks_get_tables(const fks_ctx* h, double* a_host, double* b_host, double* dirs_host, double* w_host);
 
 /* Test-only: the per-axis whole-cell shifts delta[3][N] of the most recent transport step (host). */
 fks_status fks_get_last_shift(const fks_ctx* h, int* delta_host);
+
+/* Instrumentation (bench.py): when enabled, CUDA events are recorded on the launch stream around each phase:
+ *   0 = transport gather (a1), 1 = forward transform (a2), 2 = term loop / hot kernel (a3-a5),
+ *   3 = back transform + write-back / Euler (a6-a7).
+ * fks_profile_read synchronises those events and returns, per phase, the summed milliseconds ms[4] and the
+ * number of timed launches count[4], then resets the accumulators. */
+fks_status fks_profile(fks_ctx* h, int enable);
+fks_status fks_profile_read(fks_ctx* h, double* ms, long long* count);
 
 /* Number of kernel launches issued by this handle since creation (instrumentation for the bench). */
 long long fks_launch_count(const fks_ctx* h);

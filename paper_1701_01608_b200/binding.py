@@ -21,9 +21,9 @@ STATUS_NAMES = {0: "FKS_OK", 1: "FKS_ERR_INVALID", 2: "FKS_ERR_UNSUPPORTED", 3: 
 
 #: every symbol include/fks.h declares (checked by tests/test_abi.py)
 EXPORTS = ["fks_collision_init", "fks_collision_init_ex", "fks_collision_batch", "fks_collision_batch_host",
-           "fks_transport_setup", "fks_transport_step", "fks_step", "fks_step_host", "fks_get_info",
-           "fks_get_tables", "fks_get_last_shift", "fks_launch_count", "fks_sync", "fks_destroy",
-           "fks_last_error"]
+           "fks_transport_setup", "fks_transport_step", "fks_step", "fks_step_host", "fks_get_info", "fks_get_path",
+           "fks_get_tables", "fks_get_last_shift", "fks_profile", "fks_profile_read", "fks_launch_count",
+           "fks_sync", "fks_destroy", "fks_last_error"]
 
 
 class fks_params(C.Structure):
@@ -64,8 +64,11 @@ def load_library(path: str = LIB_PATH):
         "fks_step": ([vp, vp, vp, d, vp], i),
         "fks_step_host": ([vp, vp, vp, d], i),
         "fks_get_info": ([vp, C.POINTER(i), C.POINTER(i), dp, dp], i),
+        "fks_get_path": ([vp], i),
         "fks_get_tables": ([vp, vp, vp, vp, vp], i),
         "fks_get_last_shift": ([vp, vp], i),
+        "fks_profile": ([vp, i], i),
+        "fks_profile_read": ([vp, dp, C.POINTER(ll)], i),
         "fks_launch_count": ([vp], ll),
         "fks_sync": ([vp, vp], i),
         "fks_destroy": ([vp], None),
@@ -154,6 +157,10 @@ def fks_get_info(h: int) -> dict:
     return {"P": P.value, "T": T.value, "R": R.value, "lambda": lam.value}
 
 
+def fks_get_path(h: int) -> int:
+    return int(load_library().fks_get_path(h))
+
+
 def fks_get_tables(h: int, N: int, n_dirs: int):
     import numpy as np
     info = fks_get_info(h)
@@ -171,6 +178,18 @@ def fks_get_last_shift(h: int, N: int):
     d = np.empty((3, N), dtype=np.int32)
     _check(load_library().fks_get_last_shift(h, d.ctypes.data))
     return d
+
+
+def fks_profile(h: int, enable: bool = True):
+    _check(load_library().fks_profile(h, 1 if enable else 0))
+
+
+def fks_profile_read(h: int):
+    """Per-phase (transport, forward, term loop, back) summed event milliseconds and launch counts."""
+    ms = (C.c_double * 4)()
+    cnt = (C.c_longlong * 4)()
+    _check(load_library().fks_profile_read(h, ms, cnt))
+    return list(ms), list(cnt)
 
 
 def fks_launch_count(h: int) -> int:
@@ -197,6 +216,7 @@ class Collision:
         self.N = N
         self.h = fks_collision_init_ex(N=N, L=L, M_angles=M_angles, M_radial=M_radial, kernel=kernel, **kw)
         self.info = fks_get_info(self.h)
+        self.info["path"] = fks_get_path(self.h)
 
     def collision_batch(self, f, Q=None, stream=None):
         import torch

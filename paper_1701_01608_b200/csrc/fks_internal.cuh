@@ -18,6 +18,16 @@ struct Shift {
   int delta[3][kMaxN];
 };
 
+// CUDA-event phase timers (fks_profile).  Phases: 0 transport, 1 forward, 2 term loop (hot), 3 back.
+struct PhaseTimer {
+  bool on = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> used[4];
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pool;
+  int open_phase = -1;
+  void begin(int ph, cudaStream_t st);
+  void end(int ph, cudaStream_t st);
+};
+
 struct Ctx {
   fks_params p{};
   int N = 0, K = 0, P = 0, T = 0;       // K = N-1 retained modes per axis; T separated terms (+1 loss)
@@ -27,6 +37,8 @@ struct Ctx {
   int path = FKS_PATH_AUTO;             // resolved path
   // device tables: ab[t][l] = (a_t(l), b_t(l)), t = 0..T, l flattened over K'^3
   double2* d_ab = nullptr;
+  double2* d_abT = nullptr;             // fast path: ab[t][iz][ix*K+iy] (pencil-interleaved, coalesced per lz)
+  int fast_cluster = 0;                 // fast path: CTAs per cell (thread-block cluster size)
   std::vector<double> dirs, w;          // host copy of directions / weights
   std::vector<double> kappa;            // exact power-of-two balance per term (device tables hold a*kappa, b/kappa)
   // twiddles e^{+2 pi i m/M} for M = N and M = P
@@ -48,6 +60,7 @@ struct Ctx {
   std::vector<long long> offsets;       // [3][N] in units of 1/(N*cfl_den) cell
   Shift last{};
   long long launches = 0;
+  PhaseTimer prof;
   int num_sms = 148;
 };
 
@@ -67,6 +80,10 @@ fks_status build_tables(Ctx& c);
 fks_status generic_collision(Ctx& c, const double* fin, double* out, long long n_cells, bool euler, double s,
                              cudaStream_t st);
 size_t generic_ws_bytes_per_cell(const Ctx& c);
+struct GenericWs { double2* hat; double2* a; double2* b; double* G; };
+GenericWs generic_ws(const Ctx& c, long long n);
+void generic_forward(Ctx& c, const double* fin, long long n, cudaStream_t st);
+void generic_back(Ctx& c, const double* fin, double* out, long long n, bool euler, double s, cudaStream_t st);
 
 // fast path (fast32.cu)
 bool fast_available(const Ctx& c);

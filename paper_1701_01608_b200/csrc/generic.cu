@@ -100,6 +100,59 @@ size_t generic_ws_bytes_per_cell(const Ctx& c) {
   return 16 * (K * K * K + K * K * P + K * P * P) + 8 * P * P * P;
 }
 
+GenericWs generic_ws(const Ctx& c, long long n) {
+  const long long K = c.K, P = c.P;
+  GenericWs w;
+  w.hat = reinterpret_cast<double2*>(c.d_ws);
+  w.a = w.hat + n * K * K * K;
+  w.b = w.a + n * K * K * P;
+  w.G = reinterpret_cast<double*>(w.b + n * K * P * P);
+  return w;
+}
+
+// forward transform f -> f^ into w.hat ([cell][ix][iy][iz], scaled N^-3)
+void generic_forward(Ctx& c, const double* fin, long long n, cudaStream_t st) {
+  const long long N = c.N, K = c.K;
+  const int cm = c.N / 2 - 1;
+  GenericWs w = generic_ws(c, n);
+  AxisArgs A{};
+  A.tw = c.d_twN; A.M = c.N; A.sign = -1; A.scale = 1.0;
+  A.in = fin; A.out = w.b; A.B = n * N * N; A.n_in = N; A.n_out = K; A.R = 1; A.in_off = 0; A.out_off = cm;
+  launch_axis<IN_REAL, OUT_CPLX>(c, A, st);
+  A.in = w.b; A.out = w.a; A.B = n * N; A.R = K;
+  launch_axis<IN_CPLX, OUT_CPLX>(c, A, st);
+  A.in = w.a; A.out = w.hat; A.B = n; A.R = K * K; A.scale = 1.0 / (double)(N * N * N);
+  launch_axis<IN_CPLX, OUT_CPLX>(c, A, st);
+}
+
+// back transform of w.G ([cell][px][py][pz]) to Q^ on K' (Galerkin projection), then Q (+ Euler) into out
+void generic_back(Ctx& c, const double* fin, double* out, long long n, bool euler, double s, cudaStream_t st) {
+  const long long N = c.N, K = c.K, P = c.P;
+  const int cm = c.N / 2 - 1;
+  const long long nl = K * K * K;
+  GenericWs w = generic_ws(c, n);
+  AxisArgs C{};
+  C.tw = c.d_twP; C.M = c.P; C.sign = -1; C.scale = 1.0; C.in_off = 0; C.out_off = cm;
+  C.in = w.G; C.out = w.b; C.B = n * P * P; C.n_in = P; C.n_out = K; C.R = 1;
+  launch_axis<IN_REAL, OUT_CPLX>(c, C, st);
+  C.in = w.b; C.out = w.a; C.B = n * P; C.R = K;
+  launch_axis<IN_CPLX, OUT_CPLX>(c, C, st);
+  C.in = w.a; C.out = w.hat; C.B = n; C.R = K * K; C.scale = 1.0 / ((double)P * P * P);
+  launch_axis<IN_CPLX, OUT_CPLX>(c, C, st);
+  if (c.p.project_mass) {  // A24: Q^_0 := 0
+    zero_mode_kernel<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(w.hat, n, nl, ((long long)cm * K + cm) * K + cm);
+    c.launches++;
+  }
+  AxisArgs D{};
+  D.tw = c.d_twN; D.M = c.N; D.sign = +1; D.scale = 1.0; D.in_off = cm; D.out_off = 0;
+  D.in = w.hat; D.out = w.a; D.B = n * K * K; D.n_in = K; D.n_out = N; D.R = 1;
+  launch_axis<IN_CPLX, OUT_CPLX>(c, D, st);
+  D.in = w.a; D.out = w.b; D.B = n * K; D.R = N;
+  launch_axis<IN_CPLX, OUT_CPLX>(c, D, st);
+  D.in = w.b; D.out = out; D.B = n; D.R = N * N; D.euler = euler ? 1 : 0; D.s = s; D.fstar = fin;
+  launch_axis<IN_CPLX, OUT_REAL>(c, D, st);
+}
+
 fks_status generic_collision(Ctx& c, const double* fin, double* out, long long n, bool euler, double s,
                              cudaStream_t st) {
   const long long N = c.N, K = c.K, P = c.P;
@@ -111,6 +164,7 @@ fks_status generic_collision(Ctx& c, const double* fin, double* out, long long n
   double* G = reinterpret_cast<double*>(Rb + n * K * P * P);
 
   AxisArgs A{};
+  c.prof.begin(1, st);
   // ---- forward: f -> f^ -----------------------------------------------------------
   A.tw = c.d_twN; A.M = c.N; A.sign = -1; A.scale = 1.0;
   A.in = fin; A.out = Rb; A.B = n * N * N; A.n_in = N; A.n_out = K; A.R = 1; A.in_off = 0; A.out_off = cm;
@@ -120,7 +174,9 @@ fks_status generic_collision(Ctx& c, const double* fin, double* out, long long n
   A.in = Ra; A.out = Rhat; A.B = n; A.R = K * K; A.scale = 1.0 / (double)(N * N * N);
   launch_axis<IN_CPLX, OUT_CPLX>(c, A, st);
 
+  c.prof.end(1, st);
   // ---- per term: pruned inverse K' -> P, accumulate G += Re z * Im z ---------------
+  c.prof.begin(2, st);
   const long long nl = K * K * K;
   for (int t = 0; t <= c.T; t++) {
     AxisArgs B{};
@@ -134,7 +190,9 @@ fks_status generic_collision(Ctx& c, const double* fin, double* out, long long n
     launch_axis<IN_CPLX, OUT_ACC_G>(c, B, st);
   }
 
+  c.prof.end(2, st);
   // ---- back: G -> Q^ on K' (Galerkin projection), Q^ -> Q ------------------
+  c.prof.begin(3, st);
   AxisArgs C{};
   C.tw = c.d_twP; C.M = c.P; C.sign = -1; C.scale = 1.0; C.in_off = 0; C.out_off = cm;
   C.in = G; C.out = Rb; C.B = n * P * P; C.n_in = P; C.n_out = K; C.R = 1;
@@ -155,6 +213,7 @@ fks_status generic_collision(Ctx& c, const double* fin, double* out, long long n
   launch_axis<IN_CPLX, OUT_CPLX>(c, D, st);
   D.in = Rb; D.out = out; D.B = n; D.R = N * N; D.euler = euler ? 1 : 0; D.s = s; D.fstar = fin;
   launch_axis<IN_CPLX, OUT_REAL>(c, D, st);
+  c.prof.end(3, st);
   return cuda_status(cudaPeekAtLastError(), "generic collision");
 }
 

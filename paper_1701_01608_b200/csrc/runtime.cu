@@ -63,6 +63,22 @@ void gauss_legendre(int n, double a, double b, std::vector<double>& x, std::vect
   }
 }
 
+void PhaseTimer::begin(int ph, cudaStream_t st) {
+  if (!on) return;
+  std::pair<cudaEvent_t, cudaEvent_t> ev;
+  if (!pool.empty()) { ev = pool.back(); pool.pop_back(); }
+  else { cudaEventCreate(&ev.first); cudaEventCreate(&ev.second); }
+  cudaEventRecord(ev.first, st);
+  used[ph].push_back(ev);
+  open_phase = ph;
+}
+
+void PhaseTimer::end(int ph, cudaStream_t st) {
+  if (!on || used[ph].empty()) return;
+  cudaEventRecord(used[ph].back().second, st);
+  open_phase = -1;
+}
+
 static fks_status check_device_ptr(const void* p, const char* name) {
   if (!p) { set_error(std::string(name) + " is NULL"); return FKS_ERR_INVALID; }
   cudaPointerAttributes at;
@@ -263,7 +279,11 @@ fks_status fks_transport_step(fks_ctx* h, const double* f_in, double* f_out, voi
   if (overlap(f_in, bytes, f_out, bytes)) { set_error("f_out overlaps f_in"); return FKS_ERR_INVALID; }
   if ((rc = sticky_check())) return rc;
   Shift sh = advance_generic_cell(c);
-  return launch_transport_gather(c, f_in, f_out, sh, reinterpret_cast<cudaStream_t>(stream));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  c.prof.begin(0, st);
+  rc = launch_transport_gather(c, f_in, f_out, sh, st);
+  c.prof.end(0, st);
+  return rc;
 }
 
 fks_status fks_step(fks_ctx* h, const double* f_in, double* f_out, double coll_scale, void* stream) {
@@ -281,7 +301,9 @@ fks_status fks_step(fks_ctx* h, const double* f_in, double* f_out, double coll_s
   Shift sh = advance_generic_cell(c);
   if (shift_is_identity(sh)) return run_collision(c, f_in, f_out, n, true, coll_scale, st);
   // transport (exact permutation) into f_out, then collision + Euler in place on f_out
+  c.prof.begin(0, st);
   rc = launch_transport_gather(c, f_in, f_out, sh, st);
+  c.prof.end(0, st);
   if (rc) return rc;
   return run_collision(c, f_out, f_out, n, true, coll_scale, st);
 }
@@ -363,11 +385,38 @@ fks_status fks_get_tables(const fks_ctx* h, double* a_host, double* b_host, doub
   return FKS_OK;
 }
 
+int fks_get_path(const fks_ctx* h) { return h ? reinterpret_cast<const Ctx*>(h)->path : -1; }
+
 fks_status fks_get_last_shift(const fks_ctx* h, int* delta_host) {
   if (!h || !delta_host) { set_error("NULL argument"); return FKS_ERR_INVALID; }
   const Ctx& c = *reinterpret_cast<const Ctx*>(h);
   for (int a = 0; a < 3; a++)
     for (int k = 0; k < c.N; k++) delta_host[a * c.N + k] = c.last.delta[a][k];
+  return FKS_OK;
+}
+
+fks_status fks_profile(fks_ctx* h, int enable) {
+  if (!h) { set_error("NULL handle"); return FKS_ERR_INVALID; }
+  reinterpret_cast<Ctx*>(h)->prof.on = enable != 0;
+  return FKS_OK;
+}
+
+fks_status fks_profile_read(fks_ctx* h, double* ms, long long* count) {
+  if (!h || !ms || !count) { set_error("NULL argument"); return FKS_ERR_INVALID; }
+  PhaseTimer& pt = reinterpret_cast<Ctx*>(h)->prof;
+  for (int ph = 0; ph < 4; ph++) {
+    ms[ph] = 0.0;
+    count[ph] = (long long)pt.used[ph].size();
+    for (auto& ev : pt.used[ph]) {
+      cudaError_t e = cudaEventSynchronize(ev.second);
+      if (e != cudaSuccess) return cuda_status(e, "profile event");
+      float t = 0.f;
+      cudaEventElapsedTime(&t, ev.first, ev.second);
+      ms[ph] += t;
+      pt.pool.push_back(ev);
+    }
+    pt.used[ph].clear();
+  }
   return FKS_OK;
 }
 
@@ -392,6 +441,9 @@ void fks_destroy(fks_ctx* h) {
   if (c->d_stage_in) cudaFree(c->d_stage_in);
   if (c->d_stage_out) cudaFree(c->d_stage_out);
   if (c->stage_stream) cudaStreamDestroy(c->stage_stream);
+  for (int ph = 0; ph < 4; ph++)
+    for (auto& ev : c->prof.used[ph]) c->prof.pool.push_back(ev);
+  for (auto& ev : c->prof.pool) { cudaEventDestroy(ev.first); cudaEventDestroy(ev.second); }
   delete c;
 }
 

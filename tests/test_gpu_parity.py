@@ -210,3 +210,40 @@ def test_collision_config_sampled(cuda_device, name):
     ref = oracle_Q(fh, cfg_tables(name))
     assert rel_err_per_cell(Q[cells].cpu().numpy(), ref).max() <= TOL_Q
     del f, Q
+
+
+# ---------------- fast path (N = 32 fused kernel) -----------------------------------------------------------
+
+@pytest.mark.parametrize("name", ["c2", "c4"])
+def test_fast_path_vs_oracle(cuda_device, name):
+    cfg = CONFIGS[name]
+    col = make(cfg, path=B.FKS_PATH_FAST)
+    assert B.fks_get_path(col.h) == B.FKS_PATH_FAST
+    cells = [0, 1, 2, cfg.n_cells // 2 + 3, cfg.n_cells - 1]
+    f = inputs.make_f(cfg, device=cuda_device, cells=cells)
+    Q = col.collision_batch(f).cpu().numpy()
+    ref = oracle_Q(f.cpu().numpy(), cfg_tables(name))
+    assert rel_err_per_cell(Q, ref).max() <= TOL_Q
+
+
+def test_fast_path_random_and_ragged(cuda_device):
+    cfg = CONFIGS["c2"]
+    col = make(cfg, path=B.FKS_PATH_FAST)
+    f = inputs.random_field(7, 32, seed=11, signed=True).to(cuda_device)
+    Q = col.collision_batch(f).cpu().numpy()
+    ref = oracle_Q(f.cpu().numpy(), cfg_tables("c2"))
+    assert rel_err_per_cell(Q, ref).max() <= TOL_Q
+    # generic and fast paths agree on the same input (different arithmetic order only)
+    qg = make(cfg, path=B.FKS_PATH_GENERIC).collision_batch(f).cpu().numpy()
+    assert rel_err_per_cell(Q, qg).max() <= TOL_Q
+
+
+def test_fast_path_mass(cuda_device):
+    cfg = CONFIGS["c4"]
+    f = inputs.make_f(cfg, device=cuda_device, cells=list(range(16)))
+    col = make(cfg, path=B.FKS_PATH_FAST)
+    Q = col.collision_batch(f).cpu().numpy()
+    tb = cfg_tables("c4")
+    fh = f.cpu().numpy()
+    loss = np.stack([np.abs(o.loss_part(x, tb)).sum() for x in fh])
+    assert (np.abs(Q.reshape(16, -1).sum(1)) / loss).max() <= 1e-11
