@@ -326,7 +326,12 @@ __global__ void transpose_hat_kernel(const double2* __restrict__ in, double2* __
 
 bool fast_available(const Ctx& c) { return c.N == 32 && c.P == 48; }
 
-size_t fast_ws_bytes_per_cell(const Ctx& c) { return generic_ws_bytes_per_cell(c); }
+size_t xform32_ws_bytes_per_cell();
+void xform32_forward(Ctx& c, const double* fin, double2* fhT, double2* scratch, long long n, cudaStream_t st);
+void xform32_back(Ctx& c, const double* G, double2* scratch_a, double2* scratch_b, const double* fin, double* out,
+                  long long n, bool euler, double s, cudaStream_t st);
+
+size_t fast_ws_bytes_per_cell(const Ctx&) { return xform32_ws_bytes_per_cell(); }
 
 fks_status fast_prepare(Ctx& c) {
   using namespace f32;
@@ -352,16 +357,16 @@ fks_status fast_prepare(Ctx& c) {
 fks_status fast_collision(Ctx& c, const double* fin, double* out, long long n, bool euler, double s,
                           cudaStream_t st) {
   using namespace f32;
-  GenericWs w = generic_ws(c, n);
+  // workspace: f^T [n][K^3] complex | scratch [n][P*K*16] complex | G [n][P^3] fp64
+  double2* fhT = reinterpret_cast<double2*>(c.d_ws);
+  double2* scratch = fhT + n * K * NPEN;
+  double* G = reinterpret_cast<double*>(scratch + n * (long long)P * K * 16);
   c.prof.begin(1, st);
-  generic_forward(c, fin, n, st);
-  double2* fhatT = w.b;  // K*P*P >= K*K*K complex per cell
-  transpose_hat_kernel<<<(unsigned)std::min<long long>((n * K * NPEN + 255) / 256, 65535), 256, 0, st>>>(w.hat, fhatT, n);
-  c.launches++;
+  xform32_forward(c, fin, fhT, scratch, n, st);
   c.prof.end(1, st);
 
   c.prof.begin(2, st);
-  HotArgs A{fhatT, c.d_abT, w.G, c.T + 1};
+  HotArgs A{fhT, c.d_abT, G, c.T + 1};
   hot_kernel<<<(unsigned)(n * CL), NT, R_BYTES, st>>>(A);
   c.launches++;
   c.prof.end(2, st);
@@ -369,7 +374,7 @@ fks_status fast_collision(Ctx& c, const double* fin, double* out, long long n, b
   if (rc) return rc;
 
   c.prof.begin(3, st);
-  generic_back(c, fin, out, n, euler, s, st);
+  xform32_back(c, G, scratch, fhT, fin, out, n, euler, s, st);
   c.prof.end(3, st);
   return cuda_status(cudaPeekAtLastError(), "fast collision");
 }
