@@ -124,6 +124,10 @@ fks_status fks_get_last_shift(const fks_ctx* h, int* delta_host);
 fks_status fks_profile(fks_ctx* h, int enable);
 fks_status fks_profile_read(fks_ctx* h, double* ms, long long* count);
 
+/* Debug: copy up to n entries of the hot-kernel phase timestamp buffer (allocated only when the environment
+ * variable FKS_PHASE_TIMING is set at init); returns the number copied (0 when disabled). */
+long long fks_debug_timestamps(const fks_ctx* h, long long* host, long long n);
+
 /* Number of kernel launches issued by this handle since creation (instrumentation for the bench). */
 long long fks_launch_count(const fks_ctx* h);
 

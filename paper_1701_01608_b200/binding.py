@@ -22,7 +22,7 @@ STATUS_NAMES = {0: "FKS_OK", 1: "FKS_ERR_INVALID", 2: "FKS_ERR_UNSUPPORTED", 3: 
 #: every symbol include/fks.h declares (checked by tests/test_abi.py)
 EXPORTS = ["fks_collision_init", "fks_collision_init_ex", "fks_collision_batch", "fks_collision_batch_host",
            "fks_transport_setup", "fks_transport_step", "fks_step", "fks_step_host", "fks_get_info", "fks_get_path",
-           "fks_get_tables", "fks_get_last_shift", "fks_profile", "fks_profile_read", "fks_launch_count",
+           "fks_get_tables", "fks_get_last_shift", "fks_profile", "fks_profile_read", "fks_debug_timestamps", "fks_launch_count",
            "fks_sync", "fks_destroy", "fks_last_error"]
 
 
@@ -69,6 +69,7 @@ def load_library(path: str = LIB_PATH):
         "fks_get_last_shift": ([vp, vp], i),
         "fks_profile": ([vp, i], i),
         "fks_profile_read": ([vp, dp, C.POINTER(ll)], i),
+        "fks_debug_timestamps": ([vp, vp, ll], ll),
         "fks_launch_count": ([vp], ll),
         "fks_sync": ([vp, vp], i),
         "fks_destroy": ([vp], None),
@@ -190,6 +191,13 @@ def fks_profile_read(h: int):
     cnt = (C.c_longlong * 4)()
     _check(load_library().fks_profile_read(h, ms, cnt))
     return list(ms), list(cnt)
+
+
+def fks_debug_timestamps(h: int, n: int = 65536):
+    import numpy as np
+    buf = np.zeros(n, dtype=np.int64)
+    got = load_library().fks_debug_timestamps(h, buf.ctypes.data, n)
+    return buf[:got]
 
 
 def fks_launch_count(h: int) -> int:

@@ -30,7 +30,7 @@ constexpr int PL = P / CL;            // z-planes per CTA = 8
 constexpr int NT = 384;               // threads per CTA: one per (plane, py) in the X phase
 constexpr int NPEN = K * K;           // 961 pencils
 constexpr int R_ELEMS = PL * P * K;   // complex elements of the shared region (Y layout) = 11904
-constexpr int R_BYTES = R_ELEMS * 16; // 190464 B  (>= the W1 layout PL*K*K*16 = 123008 B)
+constexpr int R_BYTES = R_ELEMS * 16; // 190464 B: Y planes of this CTA in shared memory
 constexpr int Y_THREADS = PL * K;     // 248
 
 __constant__ double2 c_w48[48];       // e^{+2 pi i m/48}
@@ -43,39 +43,10 @@ __device__ __forceinline__ unsigned cluster_rank() {
 __device__ __forceinline__ void cluster_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
 __device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
 
-__device__ __forceinline__ uint32_t mapa(uint32_t laddr, unsigned rank) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(laddr), "r"(rank));
-  return r;
-}
-__device__ __forceinline__ void st_cluster(uint32_t addr, double2 v) {
-  asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(addr), "d"(v.x), "d"(v.y) : "memory");
-}
-
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
 __device__ __forceinline__ double2 cmul(double2 w, double2 a) {
   return make_double2(fma(w.x, a.x, -w.y * a.y), fma(w.x, a.y, w.y * a.x));
-}
-
-// radix-3 DIF combine for output class r: u(m) = w48^{mr} (Z(m) + w3^{-r} Z(m-16)); x[i] = Z(i - 15)
-template <int r>
-__device__ __forceinline__ void combine(const double2 (&x)[K], double2 (&u)[16]) {
-  u[0] = x[15];
-#pragma unroll
-  for (int m = 1; m < 16; m++) {
-    const double2 a = x[m + 15], b = x[m - 1];
-    if (r == 0) {
-      u[m] = cadd(a, b);
-    } else {
-      const double ci = (r == 1) ? -0.86602540378443864676 : 0.86602540378443864676;
-      double sr = fma(-0.5, b.x, a.x);
-      sr = fma(-ci, b.y, sr);
-      double si = fma(-0.5, b.y, a.y);
-      si = fma(ci, b.x, si);
-      u[m] = cmul(c_w48[(m * r) % 48], make_double2(sr, si));
-    }
-  }
 }
 
 __device__ __forceinline__ void bfly4_inv(double2& x0, double2& x1, double2& x2, double2& x3) {
@@ -110,37 +81,9 @@ __device__ __forceinline__ void fft16_inv(double2 (&u)[16]) {
   for (int q1 = 0; q1 < 4; q1++) bfly4_inv(u[4 * q1], u[4 * q1 + 1], u[4 * q1 + 2], u[4 * q1 + 3]);
 }
 
-// outputs z(3q + r), q = 0..15, of the pruned 48-point inverse transform of x
-template <int r>
-__device__ __forceinline__ void pruned48(const double2 (&x)[K], double2 (&u)[16]) {
-  combine<r>(x, u);
-  fft16_inv(u);
-}
 __device__ __forceinline__ int qslot(int q) { return 4 * (q & 3) + (q >> 2); }
 
 // ---- TMEM helpers (tcgen05) --------------------------------------------------------------------------
-__device__ __forceinline__ void tmem_ld32(uint32_t addr, uint32_t (&v)[32]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
-        "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
-        "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-      : "r"(addr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-}
-__device__ __forceinline__ void tmem_st32(uint32_t addr, const uint32_t (&v)[32]) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
-      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};"
-      ::"r"(addr), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
-        "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]),
-        "r"(v[16]), "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]),
-        "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
-      : "memory");
-}
-
 __device__ __forceinline__ void tmem_ld16(uint32_t addr, uint32_t (&v)[16]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
@@ -157,27 +100,159 @@ __device__ __forceinline__ void tmem_st16(uint32_t addr, const uint32_t (&v)[16]
       : "memory");
 }
 
+// ---- mbarrier + TMA bulk copies (global -> this CTA's shared memory) ----------------------------------
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(bar)));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(bar)),
+               "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared(bar);
+  uint32_t done = 0;
+  long long spins = 0;
+  while (!done) {
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(done) : "r"(a), "r"(parity) : "memory");
+    if (++spins > (1LL << 28)) asm volatile("trap;");  // never hang the GPU on a byte-count bug
+  }
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src), "r"(bytes),
+                 "r"((uint32_t)__cvta_generic_to_shared(bar)) : "memory");
+}
+
 struct HotArgs {
-  const double2* fhatT;  // [cell][iz][pp], pp = ix*31 + iy
-  const double2* tabT;   // [t][iz][pp]
+  const double2* fhatT;  // [cell][LHN]: lower-half pencils in per-CTA blocks (xform32.cu lh_offset)
+  const double2* tabT;   // [t][LHN]
   double* G;             // [cell][px][py][pz]
+  double2* W1;           // [cluster][2][pz][pp]: double-buffered, L2-resident exchange of the z-pass output
+  long long n_cells;
   int T1;                // T + 1 terms
+  long long* dbg;        // optional phase timestamps (tools/phase_timing.py); nullptr in production
 };
 
+constexpr int W1_BUF = P * NPEN;  // complex elements per buffer (738 KB)
+constexpr int LHN = K * (NPEN / 2 + 1);  // lower-half block layout: 14911 complex per cell / per term
+
+// Pack / unpack one complex double as 4 x 32-bit TMEM words.
+__device__ __forceinline__ void pack4(uint32_t* w, double2 v) {
+  w[0] = (uint32_t)__double2loint(v.x); w[1] = (uint32_t)__double2hiint(v.x);
+  w[2] = (uint32_t)__double2loint(v.y); w[3] = (uint32_t)__double2hiint(v.y);
+}
+__device__ __forceinline__ double2 unpack4(const uint32_t* w) {
+  return make_double2(__hiloint2double((int)w[1], (int)w[0]), __hiloint2double((int)w[3], (int)w[2]));
+}
+
+// u(m) for one output class r from a = Z(m) (m = 1..15) and b = Z(m-16)
 template <int r>
-__device__ __forceinline__ void x_accumulate(const double2 (&x)[K], uint32_t taddr, bool first) {
-  double2 u[16];
-  pruned48<r>(x, u);
+__device__ __forceinline__ double2 comb1(int m, double2 a, double2 b) {
+  if (r == 0) return cadd(a, b);
+  const double ci = (r == 1) ? -0.86602540378443864676 : 0.86602540378443864676;
+  double sr = fma(-0.5, b.x, a.x);
+  sr = fma(-ci, b.y, sr);
+  double si = fma(-0.5, b.y, a.y);
+  si = fma(ci, b.x, si);
+  return cmul(c_w48[(m * r) % 48], make_double2(sr, si));
+}
+
+// Parked-input variant: xa[j] = Z(j) for j = 0..15 in registers; Z(m-16), m = 1..15, parked in TMEM at tP
+// (4 chunks of 4 complex = 16 columns each).
+template <int r>
+__device__ __forceinline__ void combine_parked(const double2 (&xa)[16], uint32_t tP, double2 (&u)[16]) {
+  u[0] = xa[0];
 #pragma unroll
-  for (int h = 0; h < 2; h++) {  // two halves of 8 doubles (16 TMEM columns) to bound register pressure
+  for (int c = 0; c < 4; c++) {
+    uint32_t w[16];
+    tmem_ld16(tP + 16 * c, w);
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      const int m = 4 * c + k + 1;
+      if (m <= 15) u[m] = comb1<r>(m, xa[m], unpack4(w + 4 * k));
+    }
+  }
+}
+
+// Shared-memory variant: row[i] = Z(i - 15), i = 0..30
+template <int r>
+__device__ __forceinline__ void combine_smem(const double2* row, double2 (&u)[16]) {
+  u[0] = row[15];
+#pragma unroll
+  for (int m = 1; m < 16; m++) u[m] = comb1<r>(m, row[m + 15], row[m - 1]);
+}
+
+// Park b = Z(i - 15), i = 0..14, given by `get(i)`; keep xa[j] = Z(j) = input i = j + 15.
+template <typename Get>
+__device__ __forceinline__ void load_and_park(Get get, uint32_t tP, double2 (&xa)[16]) {
+#pragma unroll
+  for (int c = 0; c < 4; c++) {
+    uint32_t w[16];
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      const int i = 4 * c + k;
+      if (i < 15) pack4(w + 4 * k, get(i));
+      else { w[4 * k] = w[4 * k + 1] = w[4 * k + 2] = w[4 * k + 3] = 0u; }
+    }
+    tmem_st16(tP + 16 * c, w);
+  }
+#pragma unroll
+  for (int j = 0; j < 16; j++) xa[j] = get(15 + j);
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
+// one output class r of the z-pass of one pencil: inputs Z(i - 15) at Zs[i * ld], outputs to W1b[pz][pp]
+template <int r>
+__device__ __forceinline__ void z_task(const double2* Zs, int ld, double2* W1b, int pp, bool act) {
+  double2 u[16];
+  u[0] = Zs[15 * ld];
+#pragma unroll
+  for (int m = 1; m < 16; m++) u[m] = comb1<r>(m, Zs[(m + 15) * ld], Zs[(m - 1) * ld]);
+  fft16_inv(u);
+  if (act) {
+#pragma unroll
+    for (int q = 0; q < 16; q++) W1b[(3 * q + r) * NPEN + pp] = u[qslot(q)];
+  }
+}
+
+template <int r>
+__device__ __forceinline__ void z_out(const double2 (&xa)[16], uint32_t tP, double2* W1b, int pp, bool act) {
+  double2 u[16];
+  combine_parked<r>(xa, tP, u);
+  fft16_inv(u);
+  if (act) {
+#pragma unroll
+    for (int q = 0; q < 16; q++) W1b[(3 * q + r) * NPEN + pp] = u[qslot(q)];
+  }
+}
+
+template <int r>
+__device__ __forceinline__ void y_out(const double2 (&xa)[16], uint32_t tP, double2* Ysh, int s, int lx, bool act) {
+  double2 u[16];
+  combine_parked<r>(xa, tP, u);
+  fft16_inv(u);
+  if (act) {
+#pragma unroll
+    for (int q = 0; q < 16; q++) Ysh[(s * P + 3 * q + r) * K + lx] = u[qslot(q)];
+  }
+}
+
+template <int r>
+__device__ __forceinline__ void x_acc(const double2* row, uint32_t tG, bool first) {
+  double2 u[16];
+  combine_smem<r>(row, u);
+  fft16_inv(u);
+#pragma unroll
+  for (int h = 0; h < 2; h++) {  // two halves of 8 doubles (16 TMEM columns)
     uint32_t g[16];
-    const uint32_t a = taddr + r * 32 + h * 16;
+    const uint32_t a = tG + r * 32 + h * 16;
     if (!first) tmem_ld16(a, g);
 #pragma unroll
     for (int j = 0; j < 8; j++) {
-      const int q = 8 * h + j;
-      const double2 z = u[qslot(q)];
-      double acc = first ? z.x * z.y : fma(z.x, z.y, __hiloint2double((int)g[2 * j + 1], (int)g[2 * j]));
+      const double2 z = u[qslot(8 * h + j)];
+      const double acc = first ? z.x * z.y : fma(z.x, z.y, __hiloint2double((int)g[2 * j + 1], (int)g[2 * j]));
       g[2 * j] = (uint32_t)__double2loint(acc);
       g[2 * j + 1] = (uint32_t)__double2hiint(acc);
     }
@@ -185,35 +260,14 @@ __device__ __forceinline__ void x_accumulate(const double2 (&x)[K], uint32_t tad
   }
 }
 
-template <int r>
-__device__ __forceinline__ void z_scatter(const double2 (&x)[K], const uint32_t (&rbase)[CL], int lx, int ly) {
-  double2 u[16];
-  pruned48<r>(x, u);
-#pragma unroll
-  for (int q = 0; q < 16; q++) {
-    const int pz = 3 * q + r, d = pz / PL, s = pz % PL;
-    st_cluster(rbase[d] + (uint32_t)(((s * K + lx) * K + ly) * 16), u[qslot(q)]);
-  }
-}
-
-template <int r>
-__device__ __forceinline__ void y_store(const double2 (&x)[K], double2* R, int s, int lx) {
-  double2 u[16];
-  pruned48<r>(x, u);
-#pragma unroll
-  for (int q = 0; q < 16; q++) {
-    const int py = 3 * q + r;
-    R[(s * P + py) * K + lx] = u[qslot(q)];
-  }
-}
-
+// Persistent kernel: one 6-CTA cluster per resident cell slot, looping over cells.
 __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT, 1) hot_kernel(HotArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
-  double2* R = reinterpret_cast<double2*>(smem);
+  double2* Ysh = reinterpret_cast<double2*>(smem);  // [PL][P][K]
   __shared__ uint32_t tmem_base_sh;
   const int tid = threadIdx.x, warp = tid >> 5;
   const unsigned crank = cluster_rank();
-  const long long cell = blockIdx.x / CL;
+  const long long cid = blockIdx.x / CL, ncl = gridDim.x / CL;
 
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;"
@@ -224,86 +278,132 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT, 1) hot_kernel(H
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tbase = tmem_base_sh;
-  // thread's TMEM row: lane 32*(warp%4) + lane, 96 columns (48 doubles) at column 96*(warp/4)
-  const uint32_t taddr = tbase + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(96 * (warp >> 2));
+  // TMEM row of this thread: lane 32*(warp%4) + lane; per warp slot (warp/4): G in 96 columns, parking in 64
+  const uint32_t trow = tbase + ((uint32_t)(32 * (warp & 3)) << 16);
+  const uint32_t tG = trow + (uint32_t)(96 * (warp >> 2));
+  const uint32_t tP = trow + 288u + (uint32_t)(64 * (warp >> 2));
 
-  const int p0 = (int)(crank * NPEN) / CL, p1 = (int)((crank + 1) * NPEN) / CL;
-  const int npc = p1 - p0;
-  const uint32_t lbase = (uint32_t)__cvta_generic_to_shared(R);
-  uint32_t rbase[CL];
-#pragma unroll
-  for (int d = 0; d < CL; d++) rbase[d] = mapa(lbase, d);
-
-  // all CTAs of the cluster are running before any DSMEM traffic
-  cluster_arrive();
-  cluster_wait();
-  cluster_arrive();  // "R free" for term 0
-
+  // Hermitian pairing: CTA c stages the lower-half pencils pp in [h0, h1) (pp <= 480) and also transforms their
+  // mirrors 960 - pp = (-lx, -ly): Z(-lx,-ly,lz) = (a+ib)(lx,ly,-lz) conj(f^(lx,ly,-lz)) (a, b even; f real)
+  constexpr int NLOW = NPEN / 2 + 1;  // 481 pencils with pp <= 480 (pp = 480 is its own mirror)
+  const int h0 = (int)(crank * NLOW) / CL, h1 = (int)((crank + 1) * NLOW) / CL;
+  const int nh = h1 - h0;                       // staged pencils (80 or 81)
+  const int nmir = (h1 == NLOW) ? nh - 1 : nh;  // mirrors (the centre pencil has none)
+  double2* W1c = A.W1 + cid * 2LL * W1_BUF;
   const long long fstride = (long long)K * NPEN;
-  for (int t = 0; t < A.T1; t++) {
-    // ---------------- Z phase ----------------
-    double2 x[K];
-    const bool zact = tid < npc;
-    const int pp = p0 + tid, lx = pp / K, ly = pp - (pp / K) * K;
-    if (zact) {
-      const double2* fh = A.fhatT + cell * fstride + pp;
-      const double2* tb = A.tabT + (long long)t * fstride + pp;
-#pragma unroll
-      for (int i = 0; i < K; i++) {
-        const double2 f = __ldg(fh + i * NPEN), ab = __ldg(tb + i * NPEN);
-        x[i] = make_double2(fma(ab.x, f.x, -ab.y * f.y), fma(ab.x, f.y, ab.y * f.x));
+
+  __shared__ __align__(8) uint64_t bar;
+  if (tid == 0) mbar_init(&bar);
+  __syncthreads();
+  uint32_t parity = 0;
+  double2* stage = Ysh;  // the Y region doubles as the staging area of each phase's inputs
+  long long* dbg = (A.dbg && tid == 0) ? A.dbg + (long long)blockIdx.x * 64 : nullptr;
+  for (long long cell = cid; cell < A.n_cells; cell += ncl) {
+    for (int t = 0; t < A.T1; t++) {
+      const bool rec = dbg && cell == cid && t >= 2 && t < 6;
+      if (rec) dbg[(t - 2) * 8 + 0] = clock64();
+      double2* W1b = W1c + (t & 1) * (long long)W1_BUF;
+      // ---------------- Z phase ----------------
+      // stage f^[cell][lz][p0..p1) and table[t][lz][p0..p1) (31 contiguous runs each) into shared memory
+      __syncthreads();  // previous X phase done with the region
+      if (tid == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        const uint32_t blk = (uint32_t)(K * nh) * 16u;  // this CTA's contiguous block (lower-half layout)
+        mbar_expect(&bar, 2u * blk);
+        bulk_g2s(stage, A.fhatT + cell * (long long)LHN + K * h0, blk, &bar);
+        bulk_g2s(stage + K * nh, A.tabT + (long long)t * LHN + K * h0, blk, &bar);
       }
-    }
-    cluster_wait();  // every CTA finished reading its region for the previous term
-    if (zact) {
-      z_scatter<0>(x, rbase, lx, ly);
-      z_scatter<1>(x, rbase, lx, ly);
-      z_scatter<2>(x, rbase, lx, ly);
-    }
-    cluster_arrive();
-    cluster_wait();  // all W1 planes delivered
+      mbar_wait(&bar, parity);
+      parity ^= 1;
+      if (rec) dbg[(t - 2) * 8 + 6] = clock64();
+      // Z of the staged pencils (over the f^ stage) and of their mirrors (over the table stage): the element
+      // pair {i, 30 - i} of pencil j is handled by one thread, so the in-place writes never race.
+      for (int e = tid; e < 16 * nh; e += NT) {
+        const int i = e / nh, j = e - (e / nh) * nh, i2 = 30 - i;
+        const double2 f1 = stage[i * nh + j], a1 = stage[(K + i) * nh + j];
+        const double2 f2 = stage[i2 * nh + j], a2 = stage[(K + i2) * nh + j];
+        stage[i * nh + j] = make_double2(fma(a1.x, f1.x, -a1.y * f1.y), fma(a1.x, f1.y, a1.y * f1.x));
+        stage[i2 * nh + j] = make_double2(fma(a2.x, f2.x, -a2.y * f2.y), fma(a2.x, f2.y, a2.y * f2.x));
+        // mirror at lz index i uses (a+ib) and conj(f^) at index 30 - i
+        stage[(K + i) * nh + j] = make_double2(fma(a2.x, f2.x, a2.y * f2.y), fma(-a2.x, f2.y, a2.y * f2.x));
+        stage[(K + i2) * nh + j] = make_double2(fma(a1.x, f1.x, a1.y * f1.y), fma(-a1.x, f1.y, a1.y * f1.x));
+      }
+      __syncthreads();
+      if (rec) dbg[(t - 2) * 8 + 7] = clock64();
+      // (pencil, r) tasks, warp-uniform r: slot k = r*192 + j; j < nh: staged pencil, nh <= j < nh + nmir: mirror
+      for (int k = tid; k < 3 * 192; k += NT) {
+        const int r = k / 192, j = k - r * 192;
+        const bool act = j < nh + nmir;
+        const bool mir = j >= nh;
+        const int jj = act ? (mir ? j - nh : j) : 0;
+        const double2* Zs = stage + (mir ? K * nh : 0) + jj;
+        const int pp = mir ? (NPEN - 1) - (h0 + jj) : h0 + jj;
+        if (r == 0) z_task<0>(Zs, nh, W1b, pp, act);
+        else if (r == 1) z_task<1>(Zs, nh, W1b, pp, act);
+        else z_task<2>(Zs, nh, W1b, pp, act);
+      }
+      if (rec) dbg[(t - 2) * 8 + 1] = clock64();
+      cluster_arrive();
+      cluster_wait();  // the z-pass output of every CTA is in W1b (release/acquire at cluster scope)
+      if (rec) dbg[(t - 2) * 8 + 2] = clock64();
 
-    // ---------------- Y phase (in place) ----------------
-    const bool yact = tid < Y_THREADS;
-    const int ys = tid / K, ylx = tid - (tid / K) * K;
-    if (yact) {
-#pragma unroll
-      for (int i = 0; i < K; i++) x[i] = R[(ys * K + ylx) * K + i];
-    }
-    __syncthreads();
-    if (yact) {
-      y_store<0>(x, R, ys, ylx);
-      y_store<1>(x, R, ys, ylx);
-      y_store<2>(x, R, ys, ylx);
-    }
-    __syncthreads();
+      // ---------------- Y phase ----------------
+      // stage this CTA's 8 planes W1b[8c + s][0..961) into the region, then transform in place
+      if (tid == 0) {
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect(&bar, (uint32_t)(PL * NPEN * 16));
+        for (int sp = 0; sp < PL; sp++)
+          bulk_g2s(stage + sp * NPEN, W1b + (long long)(crank * PL + sp) * NPEN, NPEN * 16, &bar);
+      }
+      mbar_wait(&bar, parity);
+      parity ^= 1;
+      {
+        const bool act = tid < Y_THREADS;
+        const int ys = act ? tid / K : 0, ylx = act ? tid - (tid / K) * K : 0;
+        const double2* src = stage + ys * NPEN + ylx * K;
+        double2 xa[16];
+        if (warp < 8) load_and_park([&](int i) { return src[i]; }, tP, xa);
+        __syncthreads();  // every input is in registers / TMEM: the region may now receive Y
+        if (warp < 8) {
+          y_out<0>(xa, tP, Ysh, ys, ylx, act);
+          y_out<1>(xa, tP, Ysh, ys, ylx, act);
+          y_out<2>(xa, tP, Ysh, ys, ylx, act);
+        }
+      }
+      if (rec) dbg[(t - 2) * 8 + 3] = clock64();
+      __syncthreads();
+      if (rec) dbg[(t - 2) * 8 + 4] = clock64();
 
-    // ---------------- X phase ----------------
-    const int xs = tid / P, xpy = tid - (tid / P) * P;
+      // ---------------- X phase (all warps) ----------------
+      {
+        const int xs = tid / P, xpy = tid - (tid / P) * P;
+        const double2* row = Ysh + (xs * P + xpy) * K;
+        const bool first = (t == 0);
+        x_acc<0>(row, tG, first);
+        x_acc<1>(row, tG, first);
+        x_acc<2>(row, tG, first);
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      }
+      if (rec) dbg[(t - 2) * 8 + 5] = clock64();
+    }
+    // ---------------- write G[cell][px][py][pz] ----------------
+    {
+      const int xs = tid / P, xpy = tid - (tid / P) * P;
+      const int pz = (int)crank * PL + xs;
+      double* Gc = A.G + cell * (long long)(P * P * P);
 #pragma unroll
-    for (int i = 0; i < K; i++) x[i] = R[(xs * P + xpy) * K + i];
-    cluster_arrive();  // done reading the region: the next term may write into it
-    const bool first = (t == 0);
-    x_accumulate<0>(x, taddr, first);
-    x_accumulate<1>(x, taddr, first);
-    x_accumulate<2>(x, taddr, first);
-    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-  }
-  cluster_wait();
-
-  // ---------------- write G[cell][px][py][pz] ----------------
-  {
-    const int xs = tid / P, xpy = tid - (tid / P) * P;
-    const int pz = (int)crank * PL + xs;
-    double* Gc = A.G + cell * (long long)(P * P * P);
+      for (int r = 0; r < 3; r++) {
 #pragma unroll
-    for (int r = 0; r < 3; r++) {
-      uint32_t g[32];
-      tmem_ld32(taddr + r * 32, g);
+        for (int h = 0; h < 2; h++) {
+          uint32_t g[16];
+          tmem_ld16(tG + r * 32 + h * 16, g);
 #pragma unroll
-      for (int q = 0; q < 16; q++) {
-        const int px = 3 * q + r;
-        Gc[(px * P + xpy) * P + pz] = __hiloint2double((int)g[2 * q + 1], (int)g[2 * q]);
+          for (int j = 0; j < 8; j++) {
+            const int px = 3 * (8 * h + j) + r;
+            Gc[(px * P + xpy) * P + pz] = __hiloint2double((int)g[2 * j + 1], (int)g[2 * j]);
+          }
+        }
       }
     }
   }
@@ -312,21 +412,12 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT, 1) hot_kernel(H
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tbase));
 }
 
-// f^ [cell][ix][iy][iz] -> [cell][iz][ix*31+iy]
-__global__ void transpose_hat_kernel(const double2* __restrict__ in, double2* __restrict__ out, long long n) {
-  const long long total = n * K * NPEN;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
-    const long long cell = i / (K * NPEN);
-    const int rem = (int)(i - cell * K * NPEN), iz = rem / NPEN, pp = rem - iz * NPEN;
-    out[i] = in[cell * K * NPEN + (long long)pp * K + iz];
-  }
-}
-
 }  // namespace f32
 
 bool fast_available(const Ctx& c) { return c.N == 32 && c.P == 48; }
 
 size_t xform32_ws_bytes_per_cell();
+void xform32_tables_lh(const double2* ab, double2* abL, int T1);
 void xform32_forward(Ctx& c, const double* fin, double2* fhT, double2* scratch, long long n, cudaStream_t st);
 void xform32_back(Ctx& c, const double* G, double2* scratch_a, double2* scratch_b, const double* fin, double* out,
                   long long n, bool euler, double s, cudaStream_t st);
@@ -342,14 +433,26 @@ fks_status fast_prepare(Ctx& c) {
   }
   cudaError_t e = cudaMemcpyToSymbol(c_w48, w, sizeof(w));
   if (e != cudaSuccess) return cuda_status(e, "fast constants");
-  size_t n = (size_t)(c.T + 1) * K * NPEN;
+  size_t n = (size_t)(c.T + 1) * LHN;
   e = cudaMalloc(&c.d_abT, n * sizeof(double2));
   if (e != cudaSuccess) { cudaGetLastError(); return cuda_status(e, "fast table allocation"); }
-  // reuse the transpose kernel over the T+1 tables: each "cell" is one term
-  transpose_hat_kernel<<<(unsigned)std::min<size_t>((n + 255) / 256, 4096), 256>>>(c.d_ab, c.d_abT, c.T + 1);
+  xform32_tables_lh(c.d_ab, c.d_abT, c.T + 1);
   c.launches++;
   e = cudaFuncSetAttribute(hot_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, R_BYTES);
   if (e != cudaSuccess) return cuda_status(e, "fast kernel attributes");
+  // persistent grid: as many 6-CTA clusters as can be co-resident (22 on a 148-SM B200 at 190 KB smem)
+  {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(CL * 64);
+    cfg.blockDim = dim3(NT);
+    cfg.dynamicSmemBytes = R_BYTES;
+    int ncl = 0;
+    e = cudaOccupancyMaxActiveClusters(&ncl, hot_kernel, &cfg);
+    if (e != cudaSuccess || ncl <= 0) { cudaGetLastError(); ncl = 22; }
+    c.fast_ncl = ncl;
+  }
+  e = cudaMalloc(&c.d_w1, (size_t)c.fast_ncl * 2 * W1_BUF * sizeof(double2));
+  if (e != cudaSuccess) { cudaGetLastError(); return cuda_status(e, "fast exchange buffer"); }
   c.fast_cluster = CL;
   return cuda_status(cudaDeviceSynchronize(), "fast prepare");
 }
@@ -366,8 +469,9 @@ fks_status fast_collision(Ctx& c, const double* fin, double* out, long long n, b
   c.prof.end(1, st);
 
   c.prof.begin(2, st);
-  HotArgs A{fhT, c.d_abT, G, c.T + 1};
-  hot_kernel<<<(unsigned)(n * CL), NT, R_BYTES, st>>>(A);
+  HotArgs A{fhT, c.d_abT, G, c.d_w1, n, c.T + 1, c.dbg};
+  const long long ncl = std::min<long long>(c.fast_ncl, n);
+  hot_kernel<<<(unsigned)(ncl * CL), NT, R_BYTES, st>>>(A);
   c.launches++;
   c.prof.end(2, st);
   fks_status rc = cuda_status(cudaPeekAtLastError(), "fast hot kernel launch");

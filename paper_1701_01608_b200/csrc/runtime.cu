@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include "fks_internal.cuh"
@@ -235,6 +236,10 @@ fks_status fks_collision_init_ex(fks_ctx** out, const fks_params* pp) {
     rc = fast_prepare(*c);
     if (rc) { fks_destroy(reinterpret_cast<fks_ctx*>(c)); return rc; }
   }
+  if (std::getenv("FKS_PHASE_TIMING")) {  // debug instrumentation of the hot kernel (tools/phase_timing.py)
+    if (cudaMalloc(&c->dbg, 64 * 1024 * sizeof(long long)) == cudaSuccess) cudaMemset(c->dbg, 0, 64 * 1024 * sizeof(long long));
+    else { cudaGetLastError(); c->dbg = nullptr; }
+  }
   rc = cuda_status(cudaDeviceSynchronize(), "table build");
   if (rc) { fks_destroy(reinterpret_cast<fks_ctx*>(c)); return rc; }
   *out = reinterpret_cast<fks_ctx*>(c);
@@ -420,6 +425,15 @@ fks_status fks_profile_read(fks_ctx* h, double* ms, long long* count) {
   return FKS_OK;
 }
 
+long long fks_debug_timestamps(const fks_ctx* h, long long* host, long long n) {
+  if (!h || !host) return 0;
+  const Ctx& c = *reinterpret_cast<const Ctx*>(h);
+  if (!c.dbg) return 0;
+  n = std::min<long long>(n, 64 * 1024);
+  if (cudaMemcpy(host, c.dbg, n * sizeof(long long), cudaMemcpyDeviceToHost) != cudaSuccess) { cudaGetLastError(); return 0; }
+  return n;
+}
+
 long long fks_launch_count(const fks_ctx* h) {
   return h ? reinterpret_cast<const Ctx*>(h)->launches : -1;
 }
@@ -435,6 +449,9 @@ void fks_destroy(fks_ctx* h) {
   if (!h) return;
   Ctx* c = reinterpret_cast<Ctx*>(h);
   if (c->d_ab) cudaFree(c->d_ab);
+  if (c->d_abT) cudaFree(c->d_abT);
+  if (c->d_w1) cudaFree(c->d_w1);
+  if (c->dbg) cudaFree(c->dbg);
   if (c->d_twN) cudaFree(c->d_twN);
   if (c->d_twP) cudaFree(c->d_twP);
   if (c->d_ws) cudaFree(c->d_ws);

@@ -68,6 +68,17 @@ __global__ void __launch_bounds__(256) kf1(const double* __restrict__ f, double2
   }
 }
 
+// Offset of pencil pp <= 480 (lower half of the (lx,ly) plane) at lz index iz in the per-CTA block layout used by
+// the hot kernel: CTA c of a cell's cluster owns pencils [h_c, h_{c+1}), h_c = floor(481 c / 6), stored as
+// [iz][pp - h_c] starting at 31*h_c.  One contiguous block per CTA -> one bulk copy.
+__device__ __forceinline__ int lh_offset(int pp, int iz) {
+  int c = 0;
+#pragma unroll
+  for (int k = 1; k < 6; k++) c += (pp >= (481 * k) / 6);
+  const int h0 = (481 * c) / 6, h1 = (481 * (c + 1)) / 6;
+  return K * h0 + iz * (h1 - h0) + (pp - h0);
+}
+
 __global__ void __launch_bounds__(256) kf2(const double2* __restrict__ F2, double2* __restrict__ fhT) {
   __shared__ double2 s[N * H];  // F2(jx, ly fixed, lz)
   __shared__ double2 tw[N];
@@ -80,14 +91,15 @@ __global__ void __launch_bounds__(256) kf2(const double2* __restrict__ F2, doubl
   }
   __syncthreads();
   const double sc = 1.0 / (N * N * N);
-  double2* out = fhT + cell * (long long)K * K * K;
+  double2* out = fhT + cell * (long long)K * (K * K / 2 + 1);  // lower-half pencils only (14911 per cell)
   for (int o = threadIdx.x; o < K * H; o += blockDim.x) {
     const int ix = o / H, lz = o % H, lx = ix - C;
     double2 acc = make_double2(0.0, 0.0);
     for (int jx = 0; jx < N; jx++) acc = cmac(acc, s[jx * H + lz], tw[md(lx * jx, N)]);
     acc.x *= sc; acc.y *= sc;
-    out[(long long)(lz + C) * K * K + ix * K + iy] = acc;                                                  // +l
-    if (lz > 0) out[(long long)(C - lz) * K * K + (2 * C - ix) * K + (2 * C - iy)] = make_double2(acc.x, -acc.y);  // -l
+    const int pp = ix * K + iy, pm = (K * K - 1) - pp;                        // pencil of +l and of -l
+    if (pp <= K * K / 2) out[lh_offset(pp, lz + C)] = acc;                                      // +l
+    if (lz > 0 && pm <= K * K / 2) out[lh_offset(pm, C - lz)] = make_double2(acc.x, -acc.y);    // -l
   }
 }
 
@@ -191,6 +203,27 @@ __global__ void __launch_bounds__(256) kb3(const double2* __restrict__ E1, const
 }
 
 }  // namespace x32
+
+// tables [t][ix][iy][iz] -> [t][lower-half block layout] (init only)
+__global__ void tables_to_lh_kernel(const double2* __restrict__ in, double2* __restrict__ out, int T1) {
+  using namespace x32;
+  constexpr int NL = K * (K * K / 2 + 1);
+  const long long total = (long long)T1 * NL;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
+    const long long t = e / NL;
+    const int r = (int)(e - t * NL);
+    // invert lh_offset by scanning the 6 blocks
+    int c = 0;
+    for (int k = 1; k < 6; k++) c += (r >= K * ((481 * k) / 6));
+    const int h0 = (481 * c) / 6, nh = (481 * (c + 1)) / 6 - h0;
+    const int q = r - K * h0, iz = q / nh, pp = h0 + (q - iz * nh);
+    out[e] = in[t * (long long)K * K * K + (long long)pp * K + iz];
+  }
+}
+
+void xform32_tables_lh(const double2* ab, double2* abL, int T1) {
+  tables_to_lh_kernel<<<1024, 256>>>(ab, abL, T1);
+}
 
 size_t xform32_ws_bytes_per_cell() {
   using namespace x32;
