@@ -136,13 +136,6 @@ def time_oracle(cfg, budget_s: float, max_cells: int = 256) -> dict:
 
 # ------------------------------------------------------------------------------------------------------
 
-def dist_info():
-    ws = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return ws, rank, local
-
-
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -155,9 +148,10 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
 
+    from paper_1701_01608_b200 import dist as D
     from paper_1701_01608_b200.configs import CONFIGS
     cfg = CONFIGS[args.config]
-    ws, rank, local = dist_info()
+    ws, rank, local = D.world()
     metric = "fp64 Q(f,f) cell·velocity-points/s on 1 B200; fraction of FP64/HBM roofline"
     unit = "cell·vp/s"
     workload = {"workload": f"{cfg.name}: {cfg.shape[0]}x{cfg.shape[1]}x{cfg.shape[2]} cells x {cfg.N}^3 velocities, "
@@ -203,7 +197,7 @@ def main():
 
     col = B.Collision(cfg.N, cfg.L, cfg.M, cfg.M_r, cfg.kernel)
     P, T = col.info["P"], col.info["T"]
-    fa = inputs.make_f(cfg, device=dev, seed=None if rank == 0 else rank)
+    fa = inputs.make_f(cfg, device=dev, seed=D.rank_seed(rank))
     fb = torch.empty_like(fa)
     col.transport_setup(cfg.shape, cfg.cfl_num, cfg.cfl_den)
     s = cfg.coll_scale
@@ -234,13 +228,10 @@ def main():
     launches = col.launches() - n0
     ph_ms, ph_cnt = B.fks_profile_read(col.h)
     B.fks_profile(col.h, False)
-    if ws > 1:
-        t = torch.tensor([ms_total], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_total = float(t.item())
+    ms_total = D.max_over_ranks(ms_total, dev)
     ms_step = ms_total / args.steps
     cells_all = cfg.n_cells * ws
-    value = cells_all * cfg.N ** 3 / (ms_step / 1e3)
+    value = D.weak_value(cfg.n_cells, cfg.N ** 3, ws, ms_step)
 
     # roofline of the dominant kernel (the term loop / hot kernel, phase 2)
     fl = flops_per_cell(cfg.N, P, T)
@@ -262,11 +253,7 @@ def main():
         t0 = time.perf_counter()
         for i in range(args.e2e_steps):
             B.fks_step_host(col.h, hin if i % 2 == 0 else hout, hout if i % 2 == 0 else hin, s)
-        dt = time.perf_counter() - t0
-        if ws > 1:
-            t = torch.tensor([dt], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            dt = float(t.item())
+        dt = D.max_over_ranks(time.perf_counter() - t0, dev)
         nbytes = cfg.n_cells * cfg.N ** 3 * 8
         e2e = {"value": cells_all * cfg.N ** 3 * args.e2e_steps / dt, "unit": unit,
                "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes, "steps": args.e2e_steps,

@@ -42,11 +42,12 @@ class FksError(RuntimeError):
 _lib = None
 
 
-def load_library(path: str = LIB_PATH):
+def load_library(path: str = None):
     """Load libfks.so (built in-tree by paper_1701_01608_b200/build.py).  Raises if it is missing."""
     global _lib
     if _lib is not None:
         return _lib
+    path = path or os.environ.get("FKS_LIB") or LIB_PATH
     if not os.path.exists(path):
         raise RuntimeError(f"libfks.so not found at {path}: run __graft_entry__.build() "
                            "(there is no CPU fallback)")
