@@ -283,6 +283,7 @@ def main():
         "phases_ms_per_step": {"transport": ph_ms[0] / args.steps, "forward": ph_ms[1] / args.steps,
                                "term_loop": ph_ms[2] / args.steps, "back": ph_ms[3] / args.steps},
         "path": {1: "generic", 2: "fast"}.get(col.info.get("path"), None),
+        "fast_layout": {"ctas_per_cell": col.info.get("ctas_per_cell"), "concurrent_cells": col.info.get("concurrent_cells")},
         "clocks": clocks, "gpu_launches": launches, "e2e": e2e,
         "cpu_baseline": {"value": cpu["value"], "unit": unit, "cores": oracle_threads(), "kind": "oracle",
                          "sample": f"{cpu['cells']} sampled cells of {cfg.name}, collision+Euler, "

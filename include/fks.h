@@ -109,6 +109,10 @@ fks_status fks_get_info(const fks_ctx* h, int* P, int* T, double* R, double* lam
 /* The path this handle runs (fks_path: FKS_PATH_GENERIC or FKS_PATH_FAST); -1 for a NULL handle. */
 int fks_get_path(const fks_ctx* h);
 
+/* Fast-path layout: CTAs per cell and cells processed concurrently by the persistent hot kernel (0, 0 on the
+ * generic path).  Either out pointer may be NULL. */
+fks_status fks_get_fast_layout(const fks_ctx* h, int* ctas_per_cell, int* concurrent_cells);
+
 /* Test-only: copy the tables to host arrays a_host, b_host [(T+1)][N-1][N-1][N-1], the directions
  * dirs_host [n_dirs][3] and weights w_host [n_dirs] (n_dirs = n_theta*n_phi).  Synchronous. */
 fks_status fks_get_tables(const fks_ctx* h, double* a_host, double* b_host, double* dirs_host, double* w_host);

@@ -22,6 +22,7 @@ STATUS_NAMES = {0: "FKS_OK", 1: "FKS_ERR_INVALID", 2: "FKS_ERR_UNSUPPORTED", 3: 
 #: every symbol include/fks.h declares (checked by tests/test_abi.py)
 EXPORTS = ["fks_collision_init", "fks_collision_init_ex", "fks_collision_batch", "fks_collision_batch_host",
            "fks_transport_setup", "fks_transport_step", "fks_step", "fks_step_host", "fks_get_info", "fks_get_path",
+           "fks_get_fast_layout",
            "fks_get_tables", "fks_get_last_shift", "fks_profile", "fks_profile_read", "fks_debug_timestamps", "fks_launch_count",
            "fks_sync", "fks_destroy", "fks_last_error"]
 
@@ -66,6 +67,7 @@ def load_library(path: str = None):
         "fks_step_host": ([vp, vp, vp, d], i),
         "fks_get_info": ([vp, C.POINTER(i), C.POINTER(i), dp, dp], i),
         "fks_get_path": ([vp], i),
+        "fks_get_fast_layout": ([vp, C.POINTER(i), C.POINTER(i)], i),
         "fks_get_tables": ([vp, vp, vp, vp, vp], i),
         "fks_get_last_shift": ([vp, vp], i),
         "fks_profile": ([vp, i], i),
@@ -163,6 +165,12 @@ def fks_get_path(h: int) -> int:
     return int(load_library().fks_get_path(h))
 
 
+def fks_get_fast_layout(h: int) -> dict:
+    a, b = C.c_int(), C.c_int()
+    _check(load_library().fks_get_fast_layout(h, C.byref(a), C.byref(b)))
+    return {"ctas_per_cell": a.value, "concurrent_cells": b.value}
+
+
 def fks_get_tables(h: int, N: int, n_dirs: int):
     import numpy as np
     info = fks_get_info(h)
@@ -226,6 +234,7 @@ class Collision:
         self.h = fks_collision_init_ex(N=N, L=L, M_angles=M_angles, M_radial=M_radial, kernel=kernel, **kw)
         self.info = fks_get_info(self.h)
         self.info["path"] = fks_get_path(self.h)
+        self.info.update(fks_get_fast_layout(self.h))
 
     def collision_batch(self, f, Q=None, stream=None):
         import torch

@@ -19,6 +19,8 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
+#include <string>
 #include "fks_internal.cuh"
 
 namespace fks {
@@ -412,13 +414,223 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT, 1) hot_kernel(H
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tbase));
 }
 
+
+// ======================================================================================================
+// v3: teams of 12 CTAs per cell, TWO CTAs per SM (cooperative persistent grid, global-memory team barrier).
+// Each CTA owns 4 z-planes and ~1/12 of the pencils; per SM the two resident CTAs belong to different cells,
+// so one CTA's L2 staging / barrier wait overlaps the other's FP64 work.
+// ======================================================================================================
+namespace t12 {
+constexpr int TM = 12;                      // CTAs per cell (team)
+constexpr int PL = P / TM;                  // 4 planes per CTA
+constexpr int NT = 192;                     // threads per CTA: one per (plane, py) in the X phase
+constexpr int R_BYTES = PL * P * K * 16;    // 95232 B
+constexpr int Y_THREADS = PL * K;           // 124
+constexpr int ZSLOT = 96;                   // task slots per output class (>= 41 staged + 41 mirrored pencils)
+
+struct Args {
+  const double2* fhatT;  // [cell][LHN], 12 blocks
+  const double2* tabT;   // [t][LHN], 12 blocks
+  double* G;             // [cell][px][py][pz]
+  double2* W1;           // [team][2][pz][pp]
+  unsigned* ctr;         // [team * 32]: monotonic team-barrier counters (zeroed before launch)
+  long long n_cells;
+  int T1;
+  long long* dbg;
+  long long phase_shift;  // start delay of warp group 1, in clock cycles
+};
+
+__device__ __forceinline__ void team_barrier(unsigned* ctr, unsigned target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(ctr, 1u);
+    unsigned v;
+    long long spins = 0;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+      if (++spins > (1LL << 30)) asm volatile("trap;");
+    } while (v < target);
+  }
+  __syncthreads();
+}
+
+// Group-local barrier of the 6 warps of warp group g (named barrier 1 + g; barrier 0 is __syncthreads).
+__device__ __forceinline__ void gsync(int g) { asm volatile("bar.sync %0, 192;" ::"r"(1 + g) : "memory"); }
+
+__device__ __forceinline__ void team_barrier_g(unsigned* ctr, unsigned target, int g, int ltid) {
+  gsync(g);
+  if (ltid == 0) {
+    __threadfence();
+    atomicAdd(ctr, 1u);
+    unsigned v;
+    long long spins = 0;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+      if (++spins > (1LL << 30)) asm volatile("trap;");
+    } while (v < target);
+  }
+  gsync(g);
+}
+
+// One CTA of 384 threads = two independent "virtual CTAs" (warp groups of 6 warps), each the k-th member of a
+// different team; they share the SM's TMEM (256 columns each) and shared memory (95 KB each).
+__global__ void __launch_bounds__(2 * NT, 1) hot_kernel_t12(Args A) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ uint32_t tmem_base_sh;
+  __shared__ __align__(8) uint64_t bars[2];
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int g = warp / 6, ltid = tid - g * NT, lwarp = warp - 6 * g;
+  double2* Ysh = reinterpret_cast<double2*>(smem + g * R_BYTES);  // [PL][P][K]; also the staging area
+  double2* stage = Ysh;
+  uint64_t* bar = &bars[g];
+  const int v = g * gridDim.x + blockIdx.x;  // virtual CTA id: the two groups of a CTA belong to different teams
+  const int team = v / TM, k = v - (v / TM) * TM, nteams = (2 * gridDim.x) / TM;
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;"
+                 ::"r"((uint32_t)__cvta_generic_to_shared(&tmem_base_sh)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (ltid == 0) mbar_init(bar);
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tbase = tmem_base_sh;
+  const uint32_t trow = tbase + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(256 * g);
+  const uint32_t tG = trow + (uint32_t)(96 * (lwarp >> 2));  // local warps 0-3: cols 0-95, 4-5: 96-191
+  const uint32_t tP = trow + 192u;                           // parking (Y phase: local warps 0-3 only)
+
+  constexpr int NLOW = NPEN / 2 + 1;
+  const int h0 = (k * NLOW) / TM, h1 = ((k + 1) * NLOW) / TM;
+  const int nh = h1 - h0;
+  const int nmir = (h1 == NLOW) ? nh - 1 : nh;
+  double2* W1c = A.W1 + (long long)team * 2LL * W1_BUF;
+  unsigned* ctr = A.ctr + team * 32;
+  unsigned target = 0;
+  uint32_t parity = 0;
+  long long* dbg = (A.dbg && ltid == 0) ? A.dbg + (long long)v * 64 : nullptr;
+  // Start the second warp group about half a term later so that the memory-bound Z/Y phases of one group
+  // overlap the compute-bound X phase of the other (A.phase_shift cycles; 0 disables).
+  if (g == 1 && A.phase_shift > 0) {
+    const long long t0 = clock64();
+    while (clock64() - t0 < A.phase_shift) __nanosleep(1000);
+  }
+
+  for (long long cell = team; cell < A.n_cells; cell += nteams) {
+    for (int t = 0; t < A.T1; t++) {
+      const bool rec = dbg && cell == team && t >= 2 && t < 6;
+      if (rec) dbg[(t - 2) * 8 + 0] = clock64();
+      double2* W1b = W1c + (t & 1) * (long long)W1_BUF;
+      // ---------------- Z phase ----------------
+      gsync(g);
+      if (ltid == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        const uint32_t blk = (uint32_t)(K * nh) * 16u;
+        mbar_expect(bar, 2u * blk);
+        bulk_g2s(stage, A.fhatT + cell * (long long)LHN + K * h0, blk, bar);
+        bulk_g2s(stage + K * nh, A.tabT + (long long)t * LHN + K * h0, blk, bar);
+      }
+      mbar_wait(bar, parity);
+      parity ^= 1;
+      if (rec) dbg[(t - 2) * 8 + 6] = clock64();
+      for (int e = ltid; e < 16 * nh; e += NT) {
+        const int i = e / nh, j = e - (e / nh) * nh, i2 = 30 - i;
+        const double2 f1 = stage[i * nh + j], a1 = stage[(K + i) * nh + j];
+        const double2 f2 = stage[i2 * nh + j], a2 = stage[(K + i2) * nh + j];
+        stage[i * nh + j] = make_double2(fma(a1.x, f1.x, -a1.y * f1.y), fma(a1.x, f1.y, a1.y * f1.x));
+        stage[i2 * nh + j] = make_double2(fma(a2.x, f2.x, -a2.y * f2.y), fma(a2.x, f2.y, a2.y * f2.x));
+        stage[(K + i) * nh + j] = make_double2(fma(a2.x, f2.x, a2.y * f2.y), fma(-a2.x, f2.y, a2.y * f2.x));
+        stage[(K + i2) * nh + j] = make_double2(fma(a1.x, f1.x, a1.y * f1.y), fma(-a1.x, f1.y, a1.y * f1.x));
+      }
+      gsync(g);
+      if (rec) dbg[(t - 2) * 8 + 7] = clock64();
+      for (int kk = ltid; kk < 3 * ZSLOT; kk += NT) {
+        const int r = kk / ZSLOT, j = kk - r * ZSLOT;
+        const bool act = j < nh + nmir;
+        const bool mir = j >= nh;
+        const int jj = act ? (mir ? j - nh : j) : 0;
+        const double2* Zs = stage + (mir ? K * nh : 0) + jj;
+        const int pp = mir ? (NPEN - 1) - (h0 + jj) : h0 + jj;
+        if (r == 0) z_task<0>(Zs, nh, W1b, pp, act);
+        else if (r == 1) z_task<1>(Zs, nh, W1b, pp, act);
+        else z_task<2>(Zs, nh, W1b, pp, act);
+      }
+      if (rec) dbg[(t - 2) * 8 + 1] = clock64();
+      target += TM;
+      team_barrier_g(ctr, target, g, ltid);  // every member of the team has stored its z-pass output
+      if (rec) dbg[(t - 2) * 8 + 2] = clock64();
+
+      // ---------------- Y phase ----------------
+      if (ltid == 0) {
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect(bar, (uint32_t)(PL * NPEN * 16));
+        for (int sp = 0; sp < PL; sp++)
+          bulk_g2s(stage + sp * NPEN, W1b + (long long)(k * PL + sp) * NPEN, NPEN * 16, bar);
+      }
+      mbar_wait(bar, parity);
+      parity ^= 1;
+      {
+        const bool act = ltid < Y_THREADS;
+        const int ys = act ? ltid / K : 0, ylx = act ? ltid - (ltid / K) * K : 0;
+        const double2* src = stage + ys * NPEN + ylx * K;
+        double2 xa[16];
+        if (lwarp < 4) load_and_park([&](int i) { return src[i]; }, tP, xa);
+        gsync(g);
+        if (lwarp < 4) {
+          y_out<0>(xa, tP, Ysh, ys, ylx, act);
+          y_out<1>(xa, tP, Ysh, ys, ylx, act);
+          y_out<2>(xa, tP, Ysh, ys, ylx, act);
+        }
+      }
+      if (rec) dbg[(t - 2) * 8 + 3] = clock64();
+      gsync(g);
+      if (rec) dbg[(t - 2) * 8 + 4] = clock64();
+      // ---------------- X phase ----------------
+      {
+        const int xs = ltid / P, xpy = ltid - (ltid / P) * P;
+        const double2* row = Ysh + (xs * P + xpy) * K;
+        const bool first = (t == 0);
+        x_acc<0>(row, tG, first);
+        x_acc<1>(row, tG, first);
+        x_acc<2>(row, tG, first);
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      }
+      if (rec) dbg[(t - 2) * 8 + 5] = clock64();
+    }
+    {
+      const int xs = ltid / P, xpy = ltid - (ltid / P) * P;
+      const int pz = k * PL + xs;
+      double* Gc = A.G + cell * (long long)(P * P * P);
+#pragma unroll
+      for (int r = 0; r < 3; r++) {
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          uint32_t gg[16];
+          tmem_ld16(tG + r * 32 + h * 16, gg);
+#pragma unroll
+          for (int j = 0; j < 8; j++) {
+            const int px = 3 * (8 * h + j) + r;
+            Gc[(px * P + xpy) * P + pz] = __hiloint2double((int)gg[2 * j + 1], (int)gg[2 * j]);
+          }
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tbase));
+}
+}  // namespace t12
+
 }  // namespace f32
 
 bool fast_available(const Ctx& c) { return c.N == 32 && c.P == 48; }
 
 size_t xform32_ws_bytes_per_cell();
-void xform32_tables_lh(const double2* ab, double2* abL, int T1);
-void xform32_forward(Ctx& c, const double* fin, double2* fhT, double2* scratch, long long n, cudaStream_t st);
+void xform32_tables_lh(const double2* ab, double2* abL, int T1, int nb);
+void xform32_forward(Ctx& c, const double* fin, double2* fhT, double2* scratch, long long n, int nb, cudaStream_t st);
 void xform32_back(Ctx& c, const double* G, double2* scratch_a, double2* scratch_b, const double* fin, double* out,
                   long long n, bool euler, double s, cudaStream_t st);
 
@@ -433,15 +645,32 @@ fks_status fast_prepare(Ctx& c) {
   }
   cudaError_t e = cudaMemcpyToSymbol(c_w48, w, sizeof(w));
   if (e != cudaSuccess) return cuda_status(e, "fast constants");
-  size_t n = (size_t)(c.T + 1) * LHN;
-  e = cudaMalloc(&c.d_abT, n * sizeof(double2));
-  if (e != cudaSuccess) { cudaGetLastError(); return cuda_status(e, "fast table allocation"); }
-  xform32_tables_lh(c.d_ab, c.d_abT, c.T + 1);
-  c.launches++;
   e = cudaFuncSetAttribute(hot_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, R_BYTES);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(t12::hot_kernel_t12, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * t12::R_BYTES);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(t12::hot_kernel_t12, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
   if (e != cudaSuccess) return cuda_status(e, "fast kernel attributes");
-  // persistent grid: as many 6-CTA clusters as can be co-resident (22 on a 148-SM B200 at 190 KB smem)
-  {
+  // variant: two CTAs per SM (teams of 12, default) unless FKS_HOT=c6 or the occupancy does not allow it
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, t12::hot_kernel_t12, 2 * t12::NT, 2 * t12::R_BYTES);
+  if (e != cudaSuccess) { cudaGetLastError(); per_sm = 0; }
+  if (std::getenv("FKS_DEBUG")) {
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, t12::hot_kernel_t12);
+    fprintf(stderr, "[fks] t12 occupancy per SM = %d (err %d), regs %d, static smem %zu, dyn %d, maxthreads %d\n",
+            per_sm, (int)e, fa.numRegs, fa.sharedSizeBytes, t12::R_BYTES, fa.maxThreadsPerBlock);
+
+  }
+  const char* hv = std::getenv("FKS_HOT");
+  const bool want_c6 = hv && std::string(hv) == "c6";
+  c.fast_variant = (!want_c6 && per_sm >= 1) ? t12::TM : CL;
+  size_t w1_elems;
+  if (c.fast_variant == t12::TM) {
+    c.fast_nteams = (2 * c.num_sms) / t12::TM;  // two virtual CTAs (warp groups) per SM
+    w1_elems = (size_t)c.fast_nteams * 2 * W1_BUF;
+    e = cudaMalloc(&c.d_ctr, (size_t)c.fast_nteams * 32 * sizeof(unsigned));
+    if (e != cudaSuccess) { cudaGetLastError(); return cuda_status(e, "team counters"); }
+  } else {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(CL * 64);
     cfg.blockDim = dim3(NT);
@@ -450,10 +679,15 @@ fks_status fast_prepare(Ctx& c) {
     e = cudaOccupancyMaxActiveClusters(&ncl, hot_kernel, &cfg);
     if (e != cudaSuccess || ncl <= 0) { cudaGetLastError(); ncl = 22; }
     c.fast_ncl = ncl;
+    w1_elems = (size_t)ncl * 2 * W1_BUF;
   }
-  e = cudaMalloc(&c.d_w1, (size_t)c.fast_ncl * 2 * W1_BUF * sizeof(double2));
-  if (e != cudaSuccess) { cudaGetLastError(); return cuda_status(e, "fast exchange buffer"); }
-  c.fast_cluster = CL;
+  size_t n = (size_t)(c.T + 1) * LHN;
+  e = cudaMalloc(&c.d_abT, n * sizeof(double2));
+  if (e == cudaSuccess) e = cudaMalloc(&c.d_w1, w1_elems * sizeof(double2));
+  if (e != cudaSuccess) { cudaGetLastError(); return cuda_status(e, "fast path allocation"); }
+  xform32_tables_lh(c.d_ab, c.d_abT, c.T + 1, c.fast_variant);
+  c.launches++;
+  c.fast_cluster = c.fast_variant;
   return cuda_status(cudaDeviceSynchronize(), "fast prepare");
 }
 
@@ -465,13 +699,27 @@ fks_status fast_collision(Ctx& c, const double* fin, double* out, long long n, b
   double2* scratch = fhT + n * K * NPEN;
   double* G = reinterpret_cast<double*>(scratch + n * (long long)P * K * 16);
   c.prof.begin(1, st);
-  xform32_forward(c, fin, fhT, scratch, n, st);
+  xform32_forward(c, fin, fhT, scratch, n, c.fast_variant, st);
   c.prof.end(1, st);
 
   c.prof.begin(2, st);
-  HotArgs A{fhT, c.d_abT, G, c.d_w1, n, c.T + 1, c.dbg};
-  const long long ncl = std::min<long long>(c.fast_ncl, n);
-  hot_kernel<<<(unsigned)(ncl * CL), NT, R_BYTES, st>>>(A);
+  if (c.fast_variant == t12::TM) {
+    const char* ps = std::getenv("FKS_PHASE_SHIFT");
+    t12::Args A{fhT, c.d_abT, G, c.d_w1, c.d_ctr, n, c.T + 1, c.dbg, ps ? std::atoll(ps) : 15000LL};
+    // teams are formed from the 2 * grid virtual CTAs; keep an even team count so both warp groups have work
+    long long nt = std::min<long long>(c.fast_nteams, n);
+    if (nt % 2) nt += (nt < c.fast_nteams) ? 1 : -1;
+    if (nt < 2) nt = 2;
+    cudaMemsetAsync(c.d_ctr, 0, (size_t)c.fast_nteams * 32 * sizeof(unsigned), st);
+    void* args[] = {&A};
+    cudaError_t e = cudaLaunchCooperativeKernel((void*)t12::hot_kernel_t12, dim3((unsigned)(nt * t12::TM / 2)),
+                                                dim3(2 * t12::NT), args, 2 * t12::R_BYTES, st);
+    if (e != cudaSuccess) { c.prof.end(2, st); return cuda_status(e, "cooperative hot kernel launch"); }
+  } else {
+    HotArgs A{fhT, c.d_abT, G, c.d_w1, n, c.T + 1, c.dbg};
+    const long long ncl = std::min<long long>(c.fast_ncl, n);
+    hot_kernel<<<(unsigned)(ncl * CL), NT, R_BYTES, st>>>(A);
+  }
   c.launches++;
   c.prof.end(2, st);
   fks_status rc = cuda_status(cudaPeekAtLastError(), "fast hot kernel launch");

@@ -41,7 +41,10 @@ struct Ctx {
   int fast_cluster = 0;                 // fast path: CTAs per cell (thread-block cluster size)
   int fast_ncl = 0;                     // fast path: co-resident clusters (persistent grid)
   double2* d_w1 = nullptr;
-  long long* dbg = nullptr;             // debug: hot-kernel phase timestamps (env FKS_PHASE_TIMING)              // fast path: per-cluster double-buffered z-pass exchange (L2-resident)
+  long long* dbg = nullptr;
+  int fast_variant = 6;                 // fast path: CTAs per cell (6 = cluster kernel, 12 = two-CTAs-per-SM teams)
+  int fast_nteams = 0;                  // fast path (variant 12): co-resident teams
+  unsigned* d_ctr = nullptr;            // fast path (variant 12): team-barrier counters             // debug: hot-kernel phase timestamps (env FKS_PHASE_TIMING)              // fast path: per-cluster double-buffered z-pass exchange (L2-resident)
   std::vector<double> dirs, w;          // host copy of directions / weights
   std::vector<double> kappa;            // exact power-of-two balance per term (device tables hold a*kappa, b/kappa)
   // twiddles e^{+2 pi i m/M} for M = N and M = P

@@ -390,6 +390,15 @@ fks_status fks_get_tables(const fks_ctx* h, double* a_host, double* b_host, doub
   return FKS_OK;
 }
 
+fks_status fks_get_fast_layout(const fks_ctx* h, int* ctas_per_cell, int* concurrent_cells) {
+  if (!h) { set_error("NULL handle"); return FKS_ERR_INVALID; }
+  const Ctx& c = *reinterpret_cast<const Ctx*>(h);
+  const bool fast = c.path == FKS_PATH_FAST;
+  if (ctas_per_cell) *ctas_per_cell = fast ? c.fast_variant : 0;
+  if (concurrent_cells) *concurrent_cells = fast ? (c.fast_variant == 12 ? c.fast_nteams : c.fast_ncl) : 0;
+  return FKS_OK;
+}
+
 int fks_get_path(const fks_ctx* h) { return h ? reinterpret_cast<const Ctx*>(h)->path : -1; }
 
 fks_status fks_get_last_shift(const fks_ctx* h, int* delta_host) {
@@ -452,6 +461,7 @@ void fks_destroy(fks_ctx* h) {
   if (c->d_abT) cudaFree(c->d_abT);
   if (c->d_w1) cudaFree(c->d_w1);
   if (c->dbg) cudaFree(c->dbg);
+  if (c->d_ctr) cudaFree(c->d_ctr);
   if (c->d_twN) cudaFree(c->d_twN);
   if (c->d_twP) cudaFree(c->d_twP);
   if (c->d_ws) cudaFree(c->d_ws);

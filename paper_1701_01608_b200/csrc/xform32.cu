@@ -69,17 +69,16 @@ __global__ void __launch_bounds__(256) kf1(const double* __restrict__ f, double2
 }
 
 // Offset of pencil pp <= 480 (lower half of the (lx,ly) plane) at lz index iz in the per-CTA block layout used by
-// the hot kernel: CTA c of a cell's cluster owns pencils [h_c, h_{c+1}), h_c = floor(481 c / 6), stored as
+// the hot kernel: CTA c of a cell's team of nb CTAs owns pencils [h_c, h_{c+1}), h_c = floor(481 c / nb), stored as
 // [iz][pp - h_c] starting at 31*h_c.  One contiguous block per CTA -> one bulk copy.
-__device__ __forceinline__ int lh_offset(int pp, int iz) {
+__device__ __forceinline__ int lh_offset(int pp, int iz, int nb) {
   int c = 0;
-#pragma unroll
-  for (int k = 1; k < 6; k++) c += (pp >= (481 * k) / 6);
-  const int h0 = (481 * c) / 6, h1 = (481 * (c + 1)) / 6;
+  for (int k = 1; k < nb; k++) c += (pp >= (481 * k) / nb);
+  const int h0 = (481 * c) / nb, h1 = (481 * (c + 1)) / nb;
   return K * h0 + iz * (h1 - h0) + (pp - h0);
 }
 
-__global__ void __launch_bounds__(256) kf2(const double2* __restrict__ F2, double2* __restrict__ fhT) {
+__global__ void __launch_bounds__(256) kf2(const double2* __restrict__ F2, double2* __restrict__ fhT, int nb) {
   __shared__ double2 s[N * H];  // F2(jx, ly fixed, lz)
   __shared__ double2 tw[N];
   const long long cell = blockIdx.y;
@@ -98,8 +97,8 @@ __global__ void __launch_bounds__(256) kf2(const double2* __restrict__ F2, doubl
     for (int jx = 0; jx < N; jx++) acc = cmac(acc, s[jx * H + lz], tw[md(lx * jx, N)]);
     acc.x *= sc; acc.y *= sc;
     const int pp = ix * K + iy, pm = (K * K - 1) - pp;                        // pencil of +l and of -l
-    if (pp <= K * K / 2) out[lh_offset(pp, lz + C)] = acc;                                      // +l
-    if (lz > 0 && pm <= K * K / 2) out[lh_offset(pm, C - lz)] = make_double2(acc.x, -acc.y);    // -l
+    if (pp <= K * K / 2) out[lh_offset(pp, lz + C, nb)] = acc;                                      // +l
+    if (lz > 0 && pm <= K * K / 2) out[lh_offset(pm, C - lz, nb)] = make_double2(acc.x, -acc.y);    // -l
   }
 }
 
@@ -205,24 +204,24 @@ __global__ void __launch_bounds__(256) kb3(const double2* __restrict__ E1, const
 }  // namespace x32
 
 // tables [t][ix][iy][iz] -> [t][lower-half block layout] (init only)
-__global__ void tables_to_lh_kernel(const double2* __restrict__ in, double2* __restrict__ out, int T1) {
+__global__ void tables_to_lh_kernel(const double2* __restrict__ in, double2* __restrict__ out, int T1, int nb) {
   using namespace x32;
   constexpr int NL = K * (K * K / 2 + 1);
   const long long total = (long long)T1 * NL;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
     const long long t = e / NL;
     const int r = (int)(e - t * NL);
-    // invert lh_offset by scanning the 6 blocks
+    // invert lh_offset by scanning the nb blocks
     int c = 0;
-    for (int k = 1; k < 6; k++) c += (r >= K * ((481 * k) / 6));
-    const int h0 = (481 * c) / 6, nh = (481 * (c + 1)) / 6 - h0;
+    for (int k = 1; k < nb; k++) c += (r >= K * ((481 * k) / nb));
+    const int h0 = (481 * c) / nb, nh = (481 * (c + 1)) / nb - h0;
     const int q = r - K * h0, iz = q / nh, pp = h0 + (q - iz * nh);
     out[e] = in[t * (long long)K * K * K + (long long)pp * K + iz];
   }
 }
 
-void xform32_tables_lh(const double2* ab, double2* abL, int T1) {
-  tables_to_lh_kernel<<<1024, 256>>>(ab, abL, T1);
+void xform32_tables_lh(const double2* ab, double2* abL, int T1, int nb) {
+  tables_to_lh_kernel<<<1024, 256>>>(ab, abL, T1, nb);
 }
 
 size_t xform32_ws_bytes_per_cell() {
@@ -231,12 +230,12 @@ size_t xform32_ws_bytes_per_cell() {
   return 16 * (size_t)(K * K * K + std::max(N * K * H, P * K * H)) + 8 * (size_t)P * P * P;
 }
 
-void xform32_forward(Ctx& c, const double* fin, double2* fhT, double2* scratch, long long n, cudaStream_t st) {
+void xform32_forward(Ctx& c, const double* fin, double2* fhT, double2* scratch, long long n, int nb, cudaStream_t st) {
   using namespace x32;
   for (long long c0 = 0; c0 < n; c0 += 65535) {
     const unsigned m = (unsigned)std::min<long long>(65535, n - c0);
     kf1<<<dim3(N, m), 256, 0, st>>>(fin + c0 * N * N * N, scratch + c0 * N * K * H);
-    kf2<<<dim3(K, m), 256, 0, st>>>(scratch + c0 * N * K * H, fhT + c0 * K * K * K);
+    kf2<<<dim3(K, m), 256, 0, st>>>(scratch + c0 * N * K * H, fhT + c0 * K * (K * K / 2 + 1), nb);
     c.launches += 2;
   }
 }

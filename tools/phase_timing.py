@@ -14,6 +14,7 @@ from paper_1701_01608_b200.configs import CONFIGS  # noqa: E402
 cfg = CONFIGS["c2"]
 f = inputs.make_f(cfg, device="cuda")
 col = B.Collision(cfg.N, cfg.L, cfg.M, cfg.M_r, cfg.kernel)
+print("layout", col.info)
 Q = col.collision_batch(f)
 torch.cuda.synchronize()
 raw = B.fks_debug_timestamps(col.h).reshape(-1, 64)[:, :32].reshape(-1, 4, 8)
