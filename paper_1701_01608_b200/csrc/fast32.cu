@@ -629,6 +629,7 @@ __global__ void __launch_bounds__(2 * NT, 1) hot_kernel_t12(Args A) {
 bool fast_available(const Ctx& c) { return c.N == 32 && c.P == 48; }
 
 size_t xform32_ws_bytes_per_cell();
+cudaError_t xform32_prepare();
 void xform32_tables_lh(const double2* ab, double2* abL, int T1, int nb);
 void xform32_forward(Ctx& c, const double* fin, double2* fhT, double2* scratch, long long n, int nb, cudaStream_t st);
 void xform32_back(Ctx& c, const double* G, double2* scratch_a, double2* scratch_b, const double* fin, double* out,
@@ -644,6 +645,7 @@ fks_status fast_prepare(Ctx& c) {
     w[m] = make_double2((double)cosl(a), (double)sinl(a));
   }
   cudaError_t e = cudaMemcpyToSymbol(c_w48, w, sizeof(w));
+  if (e == cudaSuccess) e = xform32_prepare();
   if (e != cudaSuccess) return cuda_status(e, "fast constants");
   e = cudaFuncSetAttribute(hot_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, R_BYTES);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(t12::hot_kernel_t12, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * t12::R_BYTES);

@@ -6,30 +6,43 @@
 
 namespace fks {
 
+// One CTA per destination cell j, 256 threads; thread t handles kz = t % N of velocity rows (kx, ky) taken
+// 256/N at a time.  The source cell of every (axis, velocity index) is resolved once per CTA in shared memory
+// (no 64-bit division in the copy loop); a warp reads a few contiguous runs (one per distinct delta_z).
 __global__ void __launch_bounds__(256) transport_gather_kernel(const double* __restrict__ fin,
                                                                double* __restrict__ fout, Shift sh) {
+  __shared__ int sx[kMaxN], sy[kMaxN], sz[kMaxN];
   const int N = sh.N;
   const long long nv = (long long)N * N * N;
-  const long long total = (long long)sh.nx * sh.ny * sh.nz * nv;
-  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
-       idx += (long long)gridDim.x * blockDim.x) {
-    const long long k = idx % nv, j = idx / nv;
-    const int kx = (int)(k / (N * N)), ky = (int)((k / N) % N), kz = (int)(k % N);
-    const int jz = (int)(j % sh.nz), jy = (int)((j / sh.nz) % sh.ny);
-    const long long jx = j / ((long long)sh.nz * sh.ny);
-    long long sx = (jx - sh.delta[0][kx]) % sh.nx; if (sx < 0) sx += sh.nx;
-    int sy = (jy - sh.delta[1][ky]) % sh.ny; if (sy < 0) sy += sh.ny;
-    int sz = (jz - sh.delta[2][kz]) % sh.nz; if (sz < 0) sz += sh.nz;
-    const long long src = (sx * sh.ny + sy) * sh.nz + sz;
-    fout[idx] = __ldg(&fin[src * nv + k]);
+  const long long j = blockIdx.x;
+  const int jz = (int)(j % sh.nz), jy = (int)((j / sh.nz) % sh.ny);
+  const int jx = (int)(j / ((long long)sh.nz * sh.ny));
+  if (threadIdx.x < N) {
+    const int k = threadIdx.x;
+    int a = (jx - sh.delta[0][k]) % sh.nx; if (a < 0) a += sh.nx;
+    int b = (jy - sh.delta[1][k]) % sh.ny; if (b < 0) b += sh.ny;
+    int c = (jz - sh.delta[2][k]) % sh.nz; if (c < 0) c += sh.nz;
+    sx[k] = a; sy[k] = b; sz[k] = c;
+  }
+  __syncthreads();
+  const int rows_per_it = 256 / N;
+  const int kz = threadIdx.x % N, rr = threadIdx.x / N;
+  if (rr >= rows_per_it) return;
+  const int czz = sz[kz];
+  double* dst = fout + j * nv;
+  for (int row = rr; row < N * N; row += rows_per_it) {
+    const int kx = row / N, ky = row - (row / N) * N;
+    const long long src = ((long long)sx[kx] * sh.ny + sy[ky]) * sh.nz + czz;
+    const long long k = (long long)row * N + kz;
+    dst[k] = __ldg(&fin[src * nv + k]);
   }
 }
 
 fks_status launch_transport_gather(Ctx& c, const double* fin, double* fout, const Shift& sh, cudaStream_t st) {
-  long long total = (long long)sh.nx * sh.ny * sh.nz * c.N * c.N * c.N;
-  long long blocks = (total + 255) / 256;
-  if (blocks > (long long)c.num_sms * 32) blocks = (long long)c.num_sms * 32;
-  transport_gather_kernel<<<(unsigned)blocks, 256, 0, st>>>(fin, fout, sh);
+  const long long cells = (long long)sh.nx * sh.ny * sh.nz;
+  if (cells == 0) return FKS_OK;
+  if (cells > 0x7fffffffLL) { set_error("transport: too many cells"); return FKS_ERR_INVALID; }
+  transport_gather_kernel<<<(unsigned)cells, 256, 0, st>>>(fin, fout, sh);
   c.launches++;
   return cuda_status(cudaPeekAtLastError(), "transport gather");
 }

@@ -3,8 +3,7 @@
 // Both use the Hermitian symmetry of real data: only the half-spectrum lz >= 0 (resp. kz >= 0) is computed and
 // the other half follows by conjugation.  Each kernel owns either a plane (two axes local in shared memory)
 // or a set of columns (the third axis), so one cell's transform is 2 (forward) or 3 (back) kernels with the
-// compact intermediates in the workspace.  The short transforms are plain DFT sums from a twiddle table in
-// shared memory (the work is < 10 % of the term loop).
+// compact intermediates in the workspace.  The short transforms are register FFTs (fft_dev.cuh).
 //
 //   forward  Kf1 plane jx : f(jx,jy,jz)  --z (real, lz=0..15)--> --y (ly in K')-->  F2[cell][jx][ly][lz]
 //            Kf2 column ly: F2(:,ly,lz)  --x (lx in K'), N^-3-->  f^T[cell][lz][lx*31+ly] and its conjugate at -l
@@ -13,6 +12,7 @@
 //            Kb3 plane jx : E1(jx,:,:)   --y inverse (jy)--> --z Hermitian->real (jz)-->  Q (or f* + s Q)
 #include <algorithm>
 #include "fks_internal.cuh"
+#include "fft_dev.cuh"
 
 namespace fks {
 namespace x32 {
@@ -20,51 +20,71 @@ namespace x32 {
 constexpr int N = 32, K = 31, P = 48, H = 16;  // H: retained non-negative z modes 0..15
 constexpr int C = N / 2 - 1;                   // mode index offset (l = i - C)
 
-// e^{sign 2 pi i m / M}
-__device__ __forceinline__ void fill_tw(double2* tw, int M, int sign) {
-  for (int m = threadIdx.x; m < M; m += blockDim.x) {
-    double s, c;
-    sincospi(2.0 * m / M, &s, &c);
-    tw[m] = make_double2(c, sign * s);
-  }
-}
-__device__ __forceinline__ double2 cmac(double2 acc, double2 x, double2 w) {
-  acc.x = fma(x.x, w.x, fma(-x.y, w.y, acc.x));
-  acc.y = fma(x.x, w.y, fma(x.y, w.x, acc.y));
-  return acc;
-}
-__device__ __forceinline__ int md(int a, int M) { a %= M; return a < 0 ? a + M : a; }
+// Each short transform below is a register FFT (fft_dev.cuh): a radix-2 (n = 32) or radix-3 (n = 48) combine of
+// one output class followed by a 16-point FFT.  One thread = one (pencil, class) task; classes are warp-uniform.
+using fftd::dif_class;
+using fftd::dif_combine;
+using fftd::fft16;
+using fftd::qslot;
+
+constexpr int PL8 = 8;  // planes (or pencil groups) per CTA in kf1 / kf2 / kb3
+constexpr int PB1 = 4;  // px planes per CTA in kb1
+constexpr int PB2 = 4;  // ky columns per CTA in kb2
+constexpr int RS = 17;  // padded row stride (double2) of 16-element rows
+constexpr int ZS = 49;  // padded row stride (double2) of 48-element rows
+
+// smem input adaptors: nz(i) is constant-folded after unrolling
+struct InCol {  // x[i] = base[i * ld], i = 0..n-1, all present
+  const double2* base; int ld;
+  __device__ __forceinline__ bool nz(int) const { return true; }
+  __device__ __forceinline__ double2 operator()(int i) const { return base[i * ld]; }
+};
+struct InModes32 {  // x[i], i = k mod 32 for k in K' (16 absent); rows stored at base[(k + C) * ld]
+  const double2* base; int ld;
+  __device__ __forceinline__ bool nz(int i) const { return i != 16; }
+  __device__ __forceinline__ double2 operator()(int i) const { return base[(i <= 15 ? i + C : i - 17) * ld]; }
+};
 
 // ---- forward ------------------------------------------------------------------------------------------
+// kf1: CTA = (cell, 8 jx planes).  z: real FFT32 per row (two reals packed per complex, FFT16, untangle),
+// lz = 0..15;  y: FFT32 over jy -> ly in K'.  Out F2[cell][jx][ly][lz].
 __global__ void __launch_bounds__(256) kf1(const double* __restrict__ f, double2* __restrict__ F2) {
-  __shared__ double sf[N * N];
-  __shared__ double2 sF1[N * H];
-  __shared__ double2 tw[N];
-  const long long cell = blockIdx.y;
-  const int jx = blockIdx.x;
-  fill_tw(tw, N, -1);
-  const double* src = f + (cell * N + jx) * N * N;
-  for (int i = threadIdx.x; i < N * N; i += blockDim.x) sf[i] = src[i];
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* buf = reinterpret_cast<double2*>(smem_raw);  // [8][32][RS] (rows padded: conflict-free row tasks)
+  const int tid = threadIdx.x;
+  const long long cell = blockIdx.x / (N / PL8);
+  const int jx0 = (blockIdx.x % (N / PL8)) * PL8;
+  const double2* src = reinterpret_cast<const double2*>(f + (cell * N + jx0) * N * N);
+#pragma unroll 4
+  for (int i = tid; i < PL8 * N * H; i += 256) buf[(i >> 4) * RS + (i & 15)] = src[i];
   __syncthreads();
-  for (int o = threadIdx.x; o < N * H; o += blockDim.x) {  // F1(jy, lz), lz = 0..15
-    const int jy = o / H, lz = o % H;
-    double2 acc = make_double2(0.0, 0.0);
-    int m = 0;
-    for (int jz = 0; jz < N; jz++) {
-      const double x = sf[jy * N + jz];
-      acc.x = fma(x, tw[m].x, acc.x);
-      acc.y = fma(x, tw[m].y, acc.y);
-      m += lz; if (m >= N) m -= N;
+  {  // z: thread = (plane, jy)
+    double2* row = buf + tid * RS;
+    double2 u[16];
+#pragma unroll
+    for (int n = 0; n < 16; n++) u[n] = row[n];
+    fft16<-1>(u);
+#pragma unroll
+    for (int k = 0; k < 16; k++) {
+      const double2 z = u[qslot(k)], zm = u[qslot((16 - k) & 15)];
+      const double2 e = make_double2(0.5 * (z.x + zm.x), 0.5 * (z.y - zm.y));   // even-sample DFT
+      const double2 o = make_double2(0.5 * (z.y + zm.y), -0.5 * (z.x - zm.x));  // odd-sample DFT
+      row[k] = k == 0 ? make_double2(e.x + o.x, 0.0) : fftd::cadd(e, fftd::cmul_s<-1>(fftd::c_tw32[k], o));
     }
-    sF1[o] = acc;
   }
   __syncthreads();
-  double2* dst = F2 + (cell * N + jx) * K * H;
-  for (int o = threadIdx.x; o < K * H; o += blockDim.x) {  // F2(ly, lz), ly in K'
-    const int iy = o / H, lz = o % H, ly = iy - C;
-    double2 acc = make_double2(0.0, 0.0);
-    for (int jy = 0; jy < N; jy++) acc = cmac(acc, sF1[jy * H + lz], tw[md(ly * jy, N)]);
-    dst[o] = acc;
+  {  // y: thread = (class r, plane, lz)
+    const int r = tid >> 7, s = (tid >> 4) & 7, lz = tid & 15;
+    InCol in{buf + s * N * RS + lz, RS};
+    double2 u[16];
+    if (r == 0) dif_class<2, -1, 0>(in, u); else dif_class<2, -1, 1>(in, u);
+    double2* dst = F2 + ((cell * N + jx0 + s) * K) * H + lz;
+#pragma unroll
+    for (int q = 0; q < 16; q++) {
+      const int k = 2 * q + r;
+      if (k == 16) continue;
+      dst[(k <= 15 ? k + C : k - 32 + C) * H] = u[qslot(q)];
+    }
   }
 }
 
@@ -78,126 +98,220 @@ __device__ __forceinline__ int lh_offset(int pp, int iz, int nb) {
   return K * h0 + iz * (h1 - h0) + (pp - h0);
 }
 
-__global__ void __launch_bounds__(256) kf2(const double2* __restrict__ F2, double2* __restrict__ fhT, int nb) {
-  __shared__ double2 s[N * H];  // F2(jx, ly fixed, lz)
-  __shared__ double2 tw[N];
-  const long long cell = blockIdx.y;
-  const int iy = blockIdx.x, ly = iy - C;
-  fill_tw(tw, N, -1);
-  for (int i = threadIdx.x; i < N * H; i += blockDim.x) {
-    const int jx = i / H, lz = i % H;
-    s[i] = F2[((cell * N + jx) * K + iy) * H + lz];
+// kf2: CTA = 8 consecutive (cell, ly) columns.  x: FFT32 over jx -> lx in K', times N^-3; writes f^ at +l and
+// (for lz > 0) its conjugate at -l, lower-half pencils only.
+__global__ void __launch_bounds__(256) kf2(const double2* __restrict__ F2, double2* __restrict__ fhT, long long ncol, int nb) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* buf = reinterpret_cast<double2*>(smem_raw);  // [8][32 jx][16 lz]
+  const int tid = threadIdx.x;
+  const long long g0 = (long long)blockIdx.x * PL8;
+#pragma unroll 4
+  for (int i = tid; i < PL8 * N * H; i += 256) {
+    const int p = i / (N * H), jx = (i / H) % N, lz = i % H;
+    const long long g = g0 + p;
+    if (g < ncol) {
+      const long long cell = g / K;
+      const int iy = (int)(g - cell * K);
+      buf[i] = F2[((cell * N + jx) * K + iy) * H + lz];
+    }
   }
   __syncthreads();
+  const int r = tid >> 7, p = (tid >> 4) & 7, lz = tid & 15;
+  const long long g = g0 + p;
+  if (g >= ncol) return;
+  const long long cell = g / K;
+  const int iy = (int)(g - cell * K);
+  InCol in{buf + p * N * H + lz, H};
+  double2 u[16];
+  if (r == 0) dif_class<2, -1, 0>(in, u); else dif_class<2, -1, 1>(in, u);
   const double sc = 1.0 / (N * N * N);
   double2* out = fhT + cell * (long long)K * (K * K / 2 + 1);  // lower-half pencils only (14911 per cell)
-  for (int o = threadIdx.x; o < K * H; o += blockDim.x) {
-    const int ix = o / H, lz = o % H, lx = ix - C;
-    double2 acc = make_double2(0.0, 0.0);
-    for (int jx = 0; jx < N; jx++) acc = cmac(acc, s[jx * H + lz], tw[md(lx * jx, N)]);
-    acc.x *= sc; acc.y *= sc;
-    const int pp = ix * K + iy, pm = (K * K - 1) - pp;                        // pencil of +l and of -l
-    if (pp <= K * K / 2) out[lh_offset(pp, lz + C, nb)] = acc;                                      // +l
-    if (lz > 0 && pm <= K * K / 2) out[lh_offset(pm, C - lz, nb)] = make_double2(acc.x, -acc.y);    // -l
+#pragma unroll
+  for (int q = 0; q < 16; q++) {
+    const int k = 2 * q + r;
+    if (k == 16) continue;
+    const int ix = k <= 15 ? k + C : k - 32 + C;
+    const double2 v = make_double2(u[qslot(q)].x * sc, u[qslot(q)].y * sc);
+    const int pp = ix * K + iy, pm = (K * K - 1) - pp;  // pencil of +l and of -l
+    if (pp <= K * K / 2) out[lh_offset(pp, lz + C, nb)] = v;
+    if (lz > 0 && pm <= K * K / 2) out[lh_offset(pm, C - lz, nb)] = make_double2(v.x, -v.y);
   }
 }
 
 // ---- back ---------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) kb1(const double* __restrict__ G, double2* __restrict__ H2) {
-  __shared__ double sg[P * P];      // G(px fixed, py, pz)  18 KB
-  __shared__ double2 sH1[P * H];    // H1(py, kz)  12 KB
-  __shared__ double2 tw[P];
-  const long long cell = blockIdx.y;
-  const int px = blockIdx.x;
-  fill_tw(tw, P, -1);
-  const double* src = G + (cell * P + px) * P * P;
-  for (int i = threadIdx.x; i < P * P; i += blockDim.x) sg[i] = src[i];
-  __syncthreads();
-  for (int o = threadIdx.x; o < P * H; o += blockDim.x) {
-    const int py = o / H, kz = o % H;
-    double2 acc = make_double2(0.0, 0.0);
-    int m = 0;
-    for (int pz = 0; pz < P; pz++) {
-      const double x = sg[py * P + pz];
-      acc.x = fma(x, tw[m].x, acc.x);
-      acc.y = fma(x, tw[m].y, acc.y);
-      m += kz; if (m >= P) m -= P;
+// kb1: CTA = (cell, 4 px planes), 288 threads.  z: two real rows packed as one complex row, FFT48, untangled
+// on the fly by the y tasks (kz = 0..15);  y: FFT48 over py -> ky in K'.  Out H2[cell][px][ky][kz].
+__global__ void __launch_bounds__(288) kb1(const double* __restrict__ G, double2* __restrict__ H2) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  // [4 planes][24 row pairs][ZS]: element pz of the pair = (G(2pr, pz), G(2pr+1, pz)); then in place the
+  // complex FFT48 of the pair
+  double2* zc = reinterpret_cast<double2*>(smem_raw);
+  const int tid = threadIdx.x;
+  const long long cell = blockIdx.x / (P / PB1);
+  const int px0 = (blockIdx.x % (P / PB1)) * PB1;
+  {
+    const double* src = G + (cell * P + px0) * P * P;
+    double* dst = reinterpret_cast<double*>(zc);
+#pragma unroll 4
+    for (int i = tid; i < PB1 * P * P; i += 288) {
+      const int row = i / P, pz = i - row * P;  // row = s * 48 + py
+      dst[((row >> 1) * ZS + pz) * 2 + (row & 1)] = src[i];
     }
-    sH1[o] = acc;
   }
   __syncthreads();
-  double2* dst = H2 + (cell * P + px) * K * H;
-  for (int o = threadIdx.x; o < K * H; o += blockDim.x) {
-    const int iy = o / H, kz = o % H, ky = iy - C;
-    double2 acc = make_double2(0.0, 0.0);
-    for (int py = 0; py < P; py++) acc = cmac(acc, sH1[py * H + kz], tw[md(ky * py, P)]);
-    dst[o] = acc;
+  {  // z: thread = (class r, plane, row pair)
+    const int r = tid / 96, s = (tid % 96) / 24, pr = tid % 24;
+    double2* zrow = zc + (s * 24 + pr) * ZS;
+    InCol in{zrow, 1};
+    double2 u[16];
+    if (r == 0) dif_combine<3, -1, 0>(in, u);
+    else if (r == 1) dif_combine<3, -1, 1>(in, u);
+    else dif_combine<3, -1, 2>(in, u);
+    __syncthreads();  // every task has read its pair: the row may now receive its transform
+    fft16<-1>(u);
+#pragma unroll
+    for (int q = 0; q < 16; q++) zrow[3 * q + r] = u[qslot(q)];
+  }
+  __syncthreads();
+  if (tid < 192) {  // y: thread = (class r, plane, kz)
+    const int r = tid >> 6, s = (tid >> 4) & 3, kz = tid & 15;
+    struct InUntangle {  // H1(py, kz): even py -> first row of the pair, odd py -> second row
+      const double2* z; int kz;
+      __device__ __forceinline__ bool nz(int) const { return true; }
+      __device__ __forceinline__ double2 operator()(int i) const {
+        const double2 a = z[(i >> 1) * ZS + kz], b = z[(i >> 1) * ZS + ((P - kz) % P)];
+        return (i & 1) ? make_double2(0.5 * (a.y + b.y), -0.5 * (a.x - b.x)) : make_double2(0.5 * (a.x + b.x), 0.5 * (a.y - b.y));
+      }
+    } in{zc + s * 24 * ZS, kz};
+    double2 u[16];
+    if (r == 0) dif_class<3, -1, 0>(in, u);
+    else if (r == 1) dif_class<3, -1, 1>(in, u);
+    else dif_class<3, -1, 2>(in, u);
+    double2* dst = H2 + ((cell * P + px0 + s) * K) * H + kz;
+#pragma unroll
+    for (int q = 0; q < 16; q++) {
+      const int k = 3 * q + r;
+      if (k >= 16 && k <= 32) continue;
+      dst[(k <= 15 ? k + C : k - 48 + C) * H] = u[qslot(q)];
+    }
   }
 }
 
-__global__ void __launch_bounds__(256) kb2(const double2* __restrict__ H2, double2* __restrict__ E1, int project_mass) {
-  __shared__ double2 s[P * H];      // H2(px, ky fixed, kz)
-  __shared__ double2 sQ[K * H];     // Q^(kx, ky fixed, kz)
-  __shared__ double2 twP[P], twN[N];
-  const long long cell = blockIdx.y;
-  const int iy = blockIdx.x, ky = iy - C;
-  fill_tw(twP, P, -1);
-  fill_tw(twN, N, +1);
-  for (int i = threadIdx.x; i < P * H; i += blockDim.x) {
-    const int px = i / H, kz = i % H;
-    s[i] = H2[((cell * P + px) * K + iy) * H + kz];
+// kb2: CTA = 4 consecutive (cell, ky) columns, 192 threads.  x: FFT48 over px -> kx in K', times P^-3
+// ([Q^_0 := 0]);  then inverse FFT32 over kx -> jx.  Out E1[cell][jx][ky][kz].
+__global__ void __launch_bounds__(192) kb2(const double2* __restrict__ H2, double2* __restrict__ E1, long long ncol,
+                                           int project_mass) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* buf = reinterpret_cast<double2*>(smem_raw);  // [4][48 px][16 kz]
+  double2* qh = buf + PB2 * P * H;                      // [4][31 kx][16 kz]
+  const int tid = threadIdx.x;
+  const long long g0 = (long long)blockIdx.x * PB2;
+#pragma unroll 4
+  for (int i = tid; i < PB2 * P * H; i += 192) {
+    const int p = i / (P * H), px = (i / H) % P, kz = i % H;
+    const long long g = g0 + p;
+    if (g < ncol) {
+      const long long cell = g / K;
+      const int iy = (int)(g - cell * K);
+      buf[i] = H2[((cell * P + px) * K + iy) * H + kz];
+    }
   }
   __syncthreads();
-  const double sc = 1.0 / ((double)P * P * P);
-  for (int o = threadIdx.x; o < K * H; o += blockDim.x) {
-    const int ix = o / H, kz = o % H, kx = ix - C;
-    double2 acc = make_double2(0.0, 0.0);
-    for (int px = 0; px < P; px++) acc = cmac(acc, s[px * H + kz], twP[md(kx * px, P)]);
-    acc.x *= sc; acc.y *= sc;
-    if (project_mass && kx == 0 && ky == 0 && kz == 0) acc = make_double2(0.0, 0.0);  // A24
-    sQ[o] = acc;
+  {
+    const int r = tid >> 6, p = (tid >> 4) & 3, kz = tid & 15;
+    const long long g = g0 + p;
+    const int iy = (int)(g % K);
+    InCol in{buf + p * P * H + kz, H};
+    double2 u[16];
+    if (r == 0) dif_class<3, -1, 0>(in, u);
+    else if (r == 1) dif_class<3, -1, 1>(in, u);
+    else dif_class<3, -1, 2>(in, u);
+    const double sc = 1.0 / ((double)P * P * P);
+#pragma unroll
+    for (int q = 0; q < 16; q++) {
+      const int k = 3 * q + r;
+      if (k >= 16 && k <= 32) continue;
+      const int ix = k <= 15 ? k + C : k - 48 + C;
+      double2 v = make_double2(u[qslot(q)].x * sc, u[qslot(q)].y * sc);
+      if (project_mass && ix == C && iy == C && kz == 0) v = make_double2(0.0, 0.0);  // A24
+      qh[(p * K + ix) * H + kz] = v;
+    }
   }
   __syncthreads();
-  double2* dst = E1 + cell * (long long)N * K * H;
-  for (int o = threadIdx.x; o < N * H; o += blockDim.x) {
-    const int jx = o / H, kz = o % H;
-    double2 acc = make_double2(0.0, 0.0);
-    for (int ix = 0; ix < K; ix++) acc = cmac(acc, sQ[ix * H + kz], twN[md((ix - C) * jx, N)]);
-    dst[(jx * K + iy) * H + kz] = acc;
+  if (tid < 128) {  // inverse x: thread = (class r, column, kz)
+    const int r = tid >> 6, p = (tid >> 4) & 3, kz = tid & 15;
+    const long long g = g0 + p;
+    if (g >= ncol) return;
+    const long long cell = g / K;
+    const int iy = (int)(g - cell * K);
+    InModes32 in{qh + p * K * H + kz, H};
+    double2 u[16];
+    if (r == 0) dif_class<2, 1, 0>(in, u); else dif_class<2, 1, 1>(in, u);
+    double2* dst = E1 + cell * (long long)N * K * H + iy * H + kz;
+#pragma unroll
+    for (int q = 0; q < 16; q++) dst[(2 * q + r) * K * H] = u[qslot(q)];
   }
 }
 
+// kb3: CTA = (cell, 8 jx planes).  y: inverse FFT32 over ky -> jy;  z: Hermitian -> real inverse FFT32 (packed
+// FFT16); then Q or f* + s Q with coalesced stores.
 __global__ void __launch_bounds__(256) kb3(const double2* __restrict__ E1, const double* fin, double* out,
                                            int euler, double s) {
-  __shared__ double2 sE[K * H];     // E1(jx fixed, ky, kz)
-  __shared__ double2 sE2[N * H];    // E2(jy, kz)
-  __shared__ double2 twN[N];
-  const long long cell = blockIdx.y;
-  const int jx = blockIdx.x;
-  fill_tw(twN, N, +1);
-  const double2* src = E1 + (cell * N + jx) * K * H;
-  for (int i = threadIdx.x; i < K * H; i += blockDim.x) sE[i] = src[i];
-  __syncthreads();
-  for (int o = threadIdx.x; o < N * H; o += blockDim.x) {
-    const int jy = o / H, kz = o % H;
-    double2 acc = make_double2(0.0, 0.0);
-    for (int iy = 0; iy < K; iy++) acc = cmac(acc, sE[iy * H + kz], twN[md((iy - C) * jy, N)]);
-    sE2[o] = acc;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* buf = reinterpret_cast<double2*>(smem_raw);  // [8][32 rows][RS]
+  const int tid = threadIdx.x;
+  const long long cell = blockIdx.x / (N / PL8);
+  const int jx0 = (blockIdx.x % (N / PL8)) * PL8;
+  {
+    const double2* src = E1 + (cell * N + jx0) * K * H;
+#pragma unroll 4
+    for (int i = tid; i < PL8 * K * H; i += 256) {
+      const int pl = i / (K * H), rem = i % (K * H);
+      buf[(pl * N + rem / H) * RS + rem % H] = src[i];
+    }
   }
   __syncthreads();
-  const long long base = (cell * N + jx) * N * N;
-  for (int o = threadIdx.x; o < N * N; o += blockDim.x) {
-    const int jy = o / N, jz = o % N;
-    // Q = Re E2(0) + 2 Re sum_{kz=1..15} E2(kz) e^{2 pi i kz jz / N}
-    double q = sE2[jy * H].x, acc = 0.0;
-    int m = jz;
-    for (int kz = 1; kz < H; kz++) {
-      const double2 e = sE2[jy * H + kz], w = twN[m];
-      acc = fma(e.x, w.x, fma(-e.y, w.y, acc));
-      m += jz; if (m >= N) m -= N;
+  {  // inverse y: thread = (class r, plane, kz)
+    const int r = tid >> 7, pl = (tid >> 4) & 7, kz = tid & 15;
+    InModes32 in{buf + pl * N * RS + kz, RS};
+    double2 u[16];
+    if (r == 0) dif_combine<2, 1, 0>(in, u); else dif_combine<2, 1, 1>(in, u);
+    __syncthreads();  // inputs consumed: write E2(jy, kz) in place
+    fft16<1>(u);
+#pragma unroll
+    for (int q = 0; q < 16; q++) buf[(pl * N + 2 * q + r) * RS + kz] = u[qslot(q)];
+  }
+  __syncthreads();
+  {  // z: thread = (plane, jy): X[k] = E2(jy, k), k = 0..15 (X[16] = 0, X[0] taken real)
+    double2* row = buf + tid * RS;
+    double2 x[16], u[16];
+#pragma unroll
+    for (int k = 0; k < 16; k++) x[k] = row[k];
+    x[0].y = 0.0;
+#pragma unroll
+    for (int k = 0; k < 16; k++) {
+      const double2 a = x[k];
+      const double2 b = k == 0 ? make_double2(0.0, 0.0) : make_double2(x[16 - k].x, -x[16 - k].y);  // conj X[16-k]
+      const double2 ev = fftd::cadd(a, b);
+      const double2 od = k == 0 ? a : fftd::cmul_s<1>(fftd::c_tw32[k], fftd::csub(a, b));
+      u[k] = make_double2(ev.x - od.y, ev.y + od.x);  // ev + i od
     }
-    q = fma(2.0, acc, q);
-    out[base + o] = euler ? fma(s, q, fin[base + o]) : q;
+    fft16<1>(u);
+#pragma unroll
+    for (int n = 0; n < 16; n++) row[n] = u[qslot(n)];  // (x[2n], x[2n+1])
+  }
+  __syncthreads();
+  const long long base = (cell * N + jx0) * N * N;
+  const double2* fi = reinterpret_cast<const double2*>(fin + base);
+  double2* o = reinterpret_cast<double2*>(out + base);
+#pragma unroll 4
+  for (int i = tid; i < PL8 * N * H; i += 256) {
+    double2 v = buf[(i >> 4) * RS + (i & 15)];
+    if (euler) {
+      const double2 a = fi[i];
+      v = make_double2(fma(s, v.x, a.x), fma(s, v.y, a.y));
+    }
+    o[i] = v;
   }
 }
 
@@ -230,27 +344,33 @@ size_t xform32_ws_bytes_per_cell() {
   return 16 * (size_t)(K * K * K + std::max(N * K * H, P * K * H)) + 8 * (size_t)P * P * P;
 }
 
+cudaError_t xform32_prepare() {
+  using namespace x32;
+  cudaError_t e = fftd::fill_twiddles();
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(kf1, cudaFuncAttributeMaxDynamicSharedMemorySize, PL8 * N * RS * 16);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(kf2, cudaFuncAttributeMaxDynamicSharedMemorySize, PL8 * N * H * 16);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(kb1, cudaFuncAttributeMaxDynamicSharedMemorySize, PB1 * 24 * ZS * 16);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(kb2, cudaFuncAttributeMaxDynamicSharedMemorySize, PB2 * (P + K) * H * 16);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(kb3, cudaFuncAttributeMaxDynamicSharedMemorySize, PL8 * N * RS * 16);
+  return e;
+}
+
 void xform32_forward(Ctx& c, const double* fin, double2* fhT, double2* scratch, long long n, int nb, cudaStream_t st) {
   using namespace x32;
-  for (long long c0 = 0; c0 < n; c0 += 65535) {
-    const unsigned m = (unsigned)std::min<long long>(65535, n - c0);
-    kf1<<<dim3(N, m), 256, 0, st>>>(fin + c0 * N * N * N, scratch + c0 * N * K * H);
-    kf2<<<dim3(K, m), 256, 0, st>>>(scratch + c0 * N * K * H, fhT + c0 * K * (K * K / 2 + 1), nb);
-    c.launches += 2;
-  }
+  const long long ncol = n * K;
+  kf1<<<(unsigned)(n * (N / PL8)), 256, PL8 * N * RS * 16, st>>>(fin, scratch);
+  kf2<<<(unsigned)((ncol + PL8 - 1) / PL8), 256, PL8 * N * H * 16, st>>>(scratch, fhT, ncol, nb);
+  c.launches += 2;
 }
 
 void xform32_back(Ctx& c, const double* G, double2* scratch_a, double2* scratch_b, const double* fin, double* out,
                   long long n, bool euler, double s, cudaStream_t st) {
   using namespace x32;
-  for (long long c0 = 0; c0 < n; c0 += 65535) {
-    const unsigned m = (unsigned)std::min<long long>(65535, n - c0);
-    kb1<<<dim3(P, m), 256, 0, st>>>(G + c0 * P * P * P, scratch_a + c0 * P * K * H);
-    kb2<<<dim3(K, m), 256, 0, st>>>(scratch_a + c0 * P * K * H, scratch_b + c0 * N * K * H, c.p.project_mass);
-    kb3<<<dim3(N, m), 256, 0, st>>>(scratch_b + c0 * N * K * H, fin + c0 * N * N * N, out + c0 * N * N * N,
-                                     euler ? 1 : 0, s);
-    c.launches += 3;
-  }
+  const long long ncol = n * K;
+  kb1<<<(unsigned)(n * (P / PB1)), 288, PB1 * 24 * ZS * 16, st>>>(G, scratch_a);
+  kb2<<<(unsigned)((ncol + PB2 - 1) / PB2), 192, PB2 * (P + K) * H * 16, st>>>(scratch_a, scratch_b, ncol, c.p.project_mass);
+  kb3<<<(unsigned)(n * (N / PL8)), 256, PL8 * N * RS * 16, st>>>(scratch_b, fin, out, euler ? 1 : 0, s);
+  c.launches += 3;
 }
 
 }  // namespace fks
