@@ -22,6 +22,7 @@
 #include <cstdlib>
 #include <string>
 #include "fks_internal.cuh"
+#include "fft_dev.cuh"
 
 namespace fks {
 namespace f32 {
@@ -130,7 +131,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 struct HotArgs {
   const double2* fhatT;  // [cell][LHN]: lower-half pencils in per-CTA blocks (xform32.cu lh_offset)
   const double2* tabT;   // [t][LHN]
-  double* G;             // [cell][px][py][pz]
+  double* G;             // [cell][px][pz][py]
   double2* W1;           // [cluster][2][pz][pp]: double-buffered, L2-resident exchange of the z-pass output
   long long n_cells;
   int T1;                // T + 1 terms
@@ -403,7 +404,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT, 1) hot_kernel(H
 #pragma unroll
           for (int j = 0; j < 8; j++) {
             const int px = 3 * (8 * h + j) + r;
-            Gc[(px * P + xpy) * P + pz] = __hiloint2double((int)g[2 * j + 1], (int)g[2 * j]);
+            Gc[(px * P + pz) * P + xpy] = __hiloint2double((int)g[2 * j + 1], (int)g[2 * j]);
           }
         }
       }
@@ -431,7 +432,7 @@ constexpr int ZSLOT = 96;                   // task slots per output class (>= 4
 struct Args {
   const double2* fhatT;  // [cell][LHN], 12 blocks
   const double2* tabT;   // [t][LHN], 12 blocks
-  double* G;             // [cell][px][py][pz]
+  double* G;             // [cell][px][pz][py]
   double2* W1;           // [team][2][pz][pp]
   unsigned* ctr;         // [team * 32]: monotonic team-barrier counters (zeroed before launch)
   long long n_cells;
@@ -612,7 +613,7 @@ __global__ void __launch_bounds__(2 * NT, 1) hot_kernel_t12(Args A) {
 #pragma unroll
           for (int j = 0; j < 8; j++) {
             const int px = 3 * (8 * h + j) + r;
-            Gc[(px * P + xpy) * P + pz] = __hiloint2double((int)gg[2 * j + 1], (int)gg[2 * j]);
+            Gc[(px * P + pz) * P + xpy] = __hiloint2double((int)gg[2 * j + 1], (int)gg[2 * j]);
           }
         }
       }
@@ -623,6 +624,695 @@ __global__ void __launch_bounds__(2 * NT, 1) hot_kernel_t12(Args A) {
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tbase));
 }
 }  // namespace t12
+
+// ======================================================================================================
+// v4: decoupled warp roles.  Teams of 12 CTAs per cell, ONE CTA per SM (4 z-planes and ~1/12 of the pencils
+// each).  Inside a CTA:
+//   * 2 Z warps produce the z-pass output W1 of term tg into a triple-buffered, L2-resident team buffer and
+//     publish it with a monotonic team counter (zdone); they run up to NB terms ahead of the consumers.
+//   * 6 YX warps form 2 groups of 3 ("pairs" of z-planes).  A group loads its two W1 planes with one TMA bulk
+//     copy per plane (prefetched during the previous term), acknowledges consumption (ydone), and runs a fixed
+//     5-round schedule synchronised only by a 96-thread named barrier:
+//        R1  Y_0(p0)  Y_0(p1)  Y_1(p0)        Y_c: y-pass of output class c (py = 3q + c), 31 lanes
+//        R2  X(0,0)   X(0,1)   X(0,2)          X(c, rx): x-pass class rx of the 32 rows of class c
+//        R3  Y_1(p1)  Y_2(p0)  Y_2(p1)         (input planes free -> prefetch W1 of the next term)
+//        R4  X(1,*)   R5  X(2,*)               G += Re z * Im z in TMEM
+//     Warp (group g, role rx) always handles px class rx, so its G accumulators (16 doubles per lane and row
+//     class) stay in its TMEM lane quarter for the whole cell.
+// ======================================================================================================
+namespace v4 {
+constexpr int TM = 12;                        // CTAs (members) per team = per cell
+constexpr int PLN = P / TM;                   // 4 z-planes per member
+constexpr int NB = 3;                         // W1 team buffers (Z warps run ahead by < NB terms)
+constexpr int NYX = 6, NZW = 2;               // YX warps (2 groups of 3), Z warps (3 Z warps cap registers at 168)
+constexpr int NTHR = 32 * (NYX + NZW);        // 288
+constexpr int NZT = 32 * NZW;                 // Z threads
+constexpr int MAXH = 41;                      // max staged pencils per member (481 / 12 rounded up)
+constexpr int ZSLOT = 96;                     // Z task slots per output class (>= 41 + 41)
+constexpr int YB = 16 * K;                    // complex elements of one Y class buffer [16 rows][31]
+constexpr int W1IN_B = NPEN * 16;             // 15376 B: one W1 plane
+constexpr int YBUF_B = YB * 16;               // 7936 B
+constexpr int PLANE_B = W1IN_B + 2 * YBUF_B;  // 31248 B per owned plane
+constexpr int ZBLK_B = K * MAXH * 16;         // 20336 B
+constexpr int OFF_Z = PLN * PLANE_B;          // 124992
+constexpr int SMEM_B = OFF_Z + 4 * ZBLK_B;    // 206336 B
+constexpr int CTR_STRIDE = 256;               // counter words per team (one 128-B line per counter)
+// Synchronisation (exact because buffer b = tg % NB is refilled only after all consumers of its previous
+// generation acknowledged it):  W1(tg) is complete when zcnt[b] == TM (tg / NB + 1);  buffer b may be
+// overwritten with W1(tg) when ycnt[b] == 2 TM (tg / NB)  (2 YX groups per member).
+
+struct Args {
+  const double2* fhatT;  // [cell][LHN], 12 blocks
+  const double2* tabT;   // [t][LHN], 12 blocks
+  double* G;             // [cell][px][pz][py]
+  double2* W1;           // [team][NB][P][NPEN]
+  unsigned* ctr;         // [team][CTR_STRIDE]: per W1 buffer b: zcnt at 32 b, ycnt at 32 (NB + b) (zeroed)
+  long long n_cells;
+  int T1;
+  int nteams;
+  long long* dbg;        // optional per-phase clock64 stamps (tools/phase_timing.py); nullptr in production
+};
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void poll_ge(const unsigned* p, unsigned target) {
+  long long spins = 0;
+  while (ld_acquire(p) < target) {
+    if (++spins > (1LL << 25)) asm volatile("trap;");  // never hang the GPU on a counting bug
+  }
+}
+__device__ __forceinline__ void nbar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+__device__ __forceinline__ void tmem_ld32(uint32_t addr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+        "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+        "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(addr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_st32(uint32_t addr, const uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};"
+      ::"r"(addr), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+        "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]),
+        "r"(v[16]), "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]),
+        "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+      : "memory");
+}
+
+// Inputs of a pruned length-48 inverse transform: modes l = -15..15 stored at base[(l + 15) * ld]; transform
+// index i = l mod 48 (16..32 absent).
+struct InK {
+  const double2* base; int ld;
+  __device__ __forceinline__ bool nz(int i) const { return i <= 15 || i >= 33; }
+  __device__ __forceinline__ double2 operator()(int i) const { return base[(i <= 15 ? i + 15 : i - 33) * ld]; }
+};
+
+// Pruned inverse transform of one output class r (runtime, warp-uniform): z(3q + r) = sum_{l=-15..15} Z(l)
+// e^{2 pi i l (3q + r)/48}, inputs Z(l) at base[(l + 15) * ld].  Radix-3 combine (only l mod 48 in 0..15 and
+// 33..47 are present) + FFT16; z(3q + r) ends in u[qslot(q)].  ONE instance per warp role keeps the kernel's hot
+// code inside the instruction cache (templated per-class copies thrashed it: ncu no_instruction stalls).
+__device__ __forceinline__ void xform48(const double2* base, int ld, int r, double2 (&u)[16]) {
+  u[0] = base[15 * ld];
+  if (r == 0) {
+#pragma unroll
+    for (int m = 1; m < 16; m++) u[m] = fftd::cadd(base[(m + 15) * ld], base[(m - 1) * ld]);
+  } else {
+    // w3^{2r} = (-1/2, -+ sin(2pi/3)) for r = 1, 2;  twiddle w48^{r m}
+    const double sg = (r == 1) ? -0.86602540378443864676 : 0.86602540378443864676;
+    const double2* tw = fftd::c_tw48;
+#pragma unroll
+    for (int m = 1; m < 16; m++) {
+      const double2 a = base[(m + 15) * ld], v = base[(m - 1) * ld];
+      double2 acc;
+      acc.x = fma(-0.5, v.x, a.x);
+      acc.x = fma(-sg, v.y, acc.x);
+      acc.y = fma(-0.5, v.y, a.y);
+      acc.y = fma(sg, v.x, acc.y);
+      u[m] = fftd::cmul_s<1>(tw[r * m], acc);
+    }
+  }
+  fftd::fft16<1>(u);
+}
+
+__global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ uint32_t tmem_base_sh;
+  __shared__ __align__(8) uint64_t bar_w1[2];
+  __shared__ __align__(8) uint64_t bar_tab, bar_fh;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int team = blockIdx.x / TM, k = blockIdx.x - (blockIdx.x / TM) * TM;
+  constexpr int NLOW = NPEN / 2 + 1;
+  const int h0 = (k * NLOW) / TM, h1 = ((k + 1) * NLOW) / TM;
+  const int nh = h1 - h0;
+  const int nmir = (h1 == NLOW) ? nh - 1 : nh;
+  double2* W1t = A.W1 + (long long)team * NB * W1_BUF;
+  unsigned* zcnt = A.ctr + (long long)team * CTR_STRIDE;  // + 32 b
+  unsigned* ycnt = zcnt + 32 * NB;                         // + 32 b
+  const long long ncell_team = (team < A.n_cells) ? (A.n_cells - 1 - team) / A.nteams + 1 : 0;
+  const long long total_tg = ncell_team * A.T1;
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;"
+                 ::"r"((uint32_t)__cvta_generic_to_shared(&tmem_base_sh)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    mbar_init(&bar_w1[0]);
+    mbar_init(&bar_w1[1]);
+    mbar_init(&bar_tab);
+    mbar_init(&bar_fh);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tbase = tmem_base_sh;
+
+  if (warp < NYX) {
+    // ---------------------------------------------- YX warps ----------------------------------------------
+    const int g = warp / 3, wr = warp - 3 * (warp / 3);
+    double2* pb0 = reinterpret_cast<double2*>(smem + (2 * g) * PLANE_B);
+    double2* pb1 = reinterpret_cast<double2*>(smem + (2 * g + 1) * PLANE_B);
+    double2* in0 = pb0;                      // W1 plane 2g
+    double2* in1 = pb1;                      // W1 plane 2g+1
+    // Y class slots: slot 0 holds row class 0 then 2, slot 1 row class 1; plane 2g at pb0, 2g+1 at pb1
+    auto ybuf = [&](int pl, int slot) { return (pl ? pb1 : pb0) + NPEN + slot * YB; };
+    const int pz0 = PLN * k + 2 * g;
+    const uint32_t tG = tbase + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(96 * g);
+    const bool leader = (wr == 0 && lane == 0);
+    auto issue_w1 = [&](long long tgi) {
+      const double2* src = W1t + (tgi % NB) * (long long)W1_BUF + (long long)pz0 * NPEN;
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_expect(&bar_w1[g], 2u * W1IN_B);
+      bulk_g2s(in0, src, W1IN_B, &bar_w1[g]);
+      bulk_g2s(in1, src + NPEN, W1IN_B, &bar_w1[g]);
+    };
+    // X rows of this lane: plane (lane >> 4), row index q = lane & 15 (py = 3q + c)
+    const int xp = lane >> 4, xq = lane & 15;
+    uint32_t par = 0;
+    bool issued = false;
+    long long tg = 0;
+#pragma unroll 1
+    for (long long cell = team; cell < A.n_cells; cell += A.nteams) {
+#pragma unroll 1
+      for (int t = 0; t < A.T1; t++, tg++) {
+        long long* st = (A.dbg && leader && g == 0 && cell == team && t >= 2 && t < 6)
+                            ? A.dbg + (long long)blockIdx.x * 128 + (t - 2) * 16 : nullptr;
+        if (st) st[0] = clock64();
+        if (leader && !issued) {
+          poll_ge(zcnt + 32 * (tg % NB), (unsigned)(TM * (tg / NB + 1)));
+          issue_w1(tg);
+        }
+        mbar_wait(&bar_w1[g], par);
+        par ^= 1;
+        if (leader) {
+          __threadfence();
+          atomicAdd(ycnt + 32 * (tg % NB), 1u);  // this group has consumed W1(tg)
+        }
+        issued = false;
+        if (st) st[1] = clock64();
+        if (t == 0) {  // zero this warp's G accumulators (3 row classes x 16 doubles per lane)
+          uint32_t zw[32];
+#pragma unroll
+          for (int i = 0; i < 32; i++) zw[i] = 0u;
+#pragma unroll
+          for (int c = 0; c < 3; c++) tmem_st32(tG + 32 * c, zw);
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        }
+#pragma unroll 1
+        for (int rd = 0; rd < 5; rd++) {
+          // task of this warp in round rd (see the schedule above)
+          const bool isx = (rd == 1 || rd == 3 || rd == 4);
+          const double2* base;
+          double2* ydst = nullptr;
+          int r;
+          uint32_t tcol = 0;
+          if (isx) {
+            const int slot = (rd == 3) ? 1 : 0;
+            base = ybuf(xp, slot) + xq * K;
+            r = wr;
+            tcol = tG + (rd == 1 ? 0u : (rd == 3 ? 32u : 64u));
+          } else {
+            // R1: (p0,c0) (p1,c0) (p0,c1);  R3: (p1,c1) (p0,c2) (p1,c2)
+            const int code = (rd == 0) ? wr : 3 + wr;
+            const int pl = (code == 1 || code == 3 || code == 5) ? 1 : 0;
+            r = (code <= 1) ? 0 : (code <= 3 ? 1 : 2);
+            const int slot = (r == 1) ? 1 : 0;
+            base = (pl ? in1 : in0) + (lane < K ? lane : K - 1) * K;
+            ydst = ybuf(pl, slot) + lane;
+          }
+          double2 u[16];
+          xform48(base, 1, r, u);
+          if (isx) {  // G(px = 3q + r, row) += Re z * Im z
+            uint32_t gw[32];
+            tmem_ld32(tcol, gw);
+#pragma unroll
+            for (int q = 0; q < 16; q++) {
+              const double2 z = u[fftd::qslot(q)];
+              const double acc = fma(z.x, z.y, __hiloint2double((int)gw[2 * q + 1], (int)gw[2 * q]));
+              gw[2 * q] = (uint32_t)__double2loint(acc);
+              gw[2 * q + 1] = (uint32_t)__double2hiint(acc);
+            }
+            tmem_st32(tcol, gw);
+          } else if (lane < K) {
+#pragma unroll
+            for (int q = 0; q < 16; q++) ydst[q * K] = u[fftd::qslot(q)];
+          }
+          if (rd == 3) continue;  // R4 -> R5: both only read
+          if (rd == 4) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+          nbar(1 + g, 96);
+          if (st) st[2 + (rd == 0 ? 0 : rd == 1 ? 1 : rd == 2 ? 2 : 3)] = clock64();
+          if (rd == 2 && leader && tg + 1 < total_tg &&
+              ld_acquire(zcnt + 32 * ((tg + 1) % NB)) >= (unsigned)(TM * ((tg + 1) / NB + 1))) {
+            issue_w1(tg + 1);  // input planes are free: overlap the copy with R4/R5
+            issued = true;
+          }
+        }
+        if (t == A.T1 - 1) {  // G[cell][px = 3q' + wr][pz][py = 3 xq + c]
+          double* Gc = A.G + cell * (long long)(P * P * P) + (long long)(pz0 + xp) * P;
+#pragma unroll
+          for (int c = 0; c < 3; c++) {
+            uint32_t gw[32];
+            tmem_ld32(tG + 32 * c, gw);
+#pragma unroll
+            for (int q = 0; q < 16; q++)
+              Gc[(long long)(3 * q + wr) * P * P + 3 * xq + c] = __hiloint2double((int)gw[2 * q + 1], (int)gw[2 * q]);
+          }
+        }
+      }
+    }
+  } else {
+    // ---------------------------------------------- Z warps -----------------------------------------------
+    const int zt = tid - 32 * NYX;  // 0..NZT-1
+    double2* fh = reinterpret_cast<double2*>(smem + OFF_Z);
+    double2* tb = reinterpret_cast<double2*>(smem + OFF_Z + ZBLK_B);
+    double2* zp = reinterpret_cast<double2*>(smem + OFF_Z + 2 * ZBLK_B);
+    double2* zm = reinterpret_cast<double2*>(smem + OFF_Z + 3 * ZBLK_B);
+    const uint32_t blk = (uint32_t)(K * nh) * 16u;
+    auto issue_tab = [&](int t) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_expect(&bar_tab, blk);
+      bulk_g2s(tb, A.tabT + (long long)t * LHN + K * h0, blk, &bar_tab);
+    };
+    auto issue_fh = [&](long long cell) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_expect(&bar_fh, blk);
+      bulk_g2s(fh, A.fhatT + cell * (long long)LHN + K * h0, blk, &bar_fh);
+    };
+    if (zt == 0 && ncell_team > 0) {
+      issue_fh(team);
+      issue_tab(0);
+    }
+    uint32_t par_tab = 0, par_fh = 0;
+    long long tg = 0;
+#pragma unroll 1
+    for (long long cell = team; cell < A.n_cells; cell += A.nteams) {
+      mbar_wait(&bar_fh, par_fh);
+      par_fh ^= 1;
+#pragma unroll 1
+      for (int t = 0; t < A.T1; t++, tg++) {
+        long long* st = (A.dbg && zt == 0 && cell == team && t >= 2 && t < 6)
+                            ? A.dbg + (long long)blockIdx.x * 128 + (t - 2) * 16 + 8 : nullptr;
+        if (st) st[0] = clock64();
+        mbar_wait(&bar_tab, par_tab);
+        par_tab ^= 1;
+        if (st) st[1] = clock64();
+        // products: Z = (a + ib) f^ for the staged pencils, and for their mirrors (-lx,-ly): (a + ib) conj(f^)
+        // at the reversed lz (a, b even; f real)
+        {  // element pairs {i, 30 - i} of pencil j, e = i * nh + j, walked without division
+          int i = zt / nh, j = zt - (zt / nh) * nh;
+#pragma unroll 2
+          for (int e = zt; e < 16 * nh; e += NZT) {
+            const int i2 = 30 - i;
+            const double2 f1 = fh[i * nh + j], a1 = tb[i * nh + j];
+            const double2 f2 = fh[i2 * nh + j], a2 = tb[i2 * nh + j];
+            zp[i * nh + j] = make_double2(fma(a1.x, f1.x, -a1.y * f1.y), fma(a1.x, f1.y, a1.y * f1.x));
+            zp[i2 * nh + j] = make_double2(fma(a2.x, f2.x, -a2.y * f2.y), fma(a2.x, f2.y, a2.y * f2.x));
+            zm[i * nh + j] = make_double2(fma(a2.x, f2.x, a2.y * f2.y), fma(-a2.x, f2.y, a2.y * f2.x));
+            zm[i2 * nh + j] = make_double2(fma(a1.x, f1.x, a1.y * f1.y), fma(-a1.x, f1.y, a1.y * f1.x));
+            j += NZT;
+            while (j >= nh) { j -= nh; i++; }
+          }
+        }
+        nbar(3, NZT);  // products complete; tb (and, after the last term, fh) free
+        if (st) st[2] = clock64();
+        if (zt == 0) {
+          if (t + 1 < A.T1) issue_tab(t + 1);
+          else if (cell + A.nteams < A.n_cells) {
+            issue_fh(cell + A.nteams);
+            issue_tab(0);
+          }
+          if (tg >= NB) poll_ge(ycnt + 32 * (tg % NB), (unsigned)(2 * TM * (tg / NB)));  // buffer free
+        }
+        nbar(3, NZT);
+        if (st) st[3] = clock64();
+        double2* W1b = W1t + (tg % NB) * (long long)W1_BUF;
+        // dense task list: tau = r * na + j (na = staged + mirrored pencils); NZT lanes x rounds cover 3 na <= 246
+        const int na = nh + nmir;
+#pragma unroll 1
+        for (int kk = zt; kk < 3 * na + NZT - 1 - ((3 * na + NZT - 1) % NZT); kk += NZT) {
+          const bool act = kk < 3 * na;
+          const int kc = act ? kk : 0;
+          const int r = kc / na, j = kc - r * na;
+          const bool mir = j >= nh;
+          const int jj = mir ? j - nh : j;
+          const double2* Zs = (mir ? zm : zp) + jj;
+          const int pp = mir ? (NPEN - 1) - (h0 + jj) : h0 + jj;
+          double2 u[16];
+          xform48(Zs, nh, r, u);
+          if (act) {
+#pragma unroll
+            for (int q = 0; q < 16; q++) W1b[(3 * q + r) * NPEN + pp] = u[fftd::qslot(q)];
+          }
+        }
+        nbar(3, NZT);
+        if (st) st[4] = clock64();
+        if (zt == 0) {
+          __threadfence();
+          atomicAdd(zcnt + 32 * (tg % NB), 1u);  // W1(tg) of this member is published
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tbase));
+}
+}  // namespace v4
+
+// ======================================================================================================
+// v5: "pencil tasks".  Same team structure as v4 (12 CTAs per cell, one CTA of 8 warps per SM, 4 z-planes and
+// ~1/12 of the pencils per CTA, triple-buffered L2 exchange with per-buffer produce/consume counters), but
+// every task loads its 31 inputs ONCE into registers and computes all three output classes from them (the
+// class-task kernels re-read each input three times from shared memory, which cost as much smem bandwidth as
+// the FP64 work).  Z products are formed on the fly (each product feeds exactly one pencil task), so there is
+// no product pass.  Two rounds per term, separated by CTA barriers:
+//     R1(t):  warps 0-3  Y(t) of plane w (31 lanes)          warp 4: Z(t+1) pencils [64, na)
+//     R2(t):  warps 0-5  X(t) of rows 32w..32w+31 (192 rows)  warps 6-7: Z(t+2) pencils [0, 64)
+// Z(t') is published (zcnt) after R1(t'-1); W1(t') is bulk-copied during R2(t'-1) and read by R1(t').
+// ======================================================================================================
+namespace v5 {
+using v4::ld_acquire;
+using v4::poll_ge;
+using v4::tmem_ld32;
+using v4::tmem_st32;
+constexpr int TM = 12, PLN = 4, NB = 3, NW = 8, NTHR = 32 * NW;
+constexpr int MAXH = 41;
+constexpr int W1IN_B = NPEN * 16;                 // 15376
+constexpr int YPL = P * K;                        // complex per plane of the Y region ([py][ix])
+constexpr int ZBLK_B = K * MAXH * 16;             // 20336
+constexpr int OFF_Y = PLN * W1IN_B;               // 61504
+constexpr int OFF_FH = OFF_Y + PLN * YPL * 16;    // 156736
+constexpr int OFF_TB = OFF_FH + ZBLK_B;           // 177072 (two buffers)
+constexpr int SMEM_B = OFF_TB + 2 * ZBLK_B;       // 217744
+constexpr int CTR_STRIDE = 256;
+constexpr int ZA = 64;                            // Z pencils done in R2 (part A); the rest in R1 (part B)
+
+struct Args {
+  const double2* fhatT;  // [cell][LHN], 12 blocks
+  const double2* tabT;   // [t][LHN], 12 blocks
+  double* G;             // [cell][px][pz][py]
+  double2* W1;           // [team][NB][P][NPEN]
+  unsigned* ctr;         // [team][CTR_STRIDE]: zcnt[b] at 32 b, ycnt[b] at 32 (NB + b)
+  long long n_cells;
+  int T1;
+  int nteams;
+  long long* dbg;
+};
+
+// u = class r of the pruned inverse 48-point transform of x (modes l = -15..15 at x[l + 15]), r warp-uniform
+__device__ __forceinline__ void xform48_regs(const double2 (&x)[K], int r, double2 (&u)[16]) {
+  u[0] = x[15];
+  if (r == 0) {
+#pragma unroll
+    for (int m = 1; m < 16; m++) u[m] = fftd::cadd(x[m + 15], x[m - 1]);
+  } else {
+    const double sg = (r == 1) ? -0.86602540378443864676 : 0.86602540378443864676;
+    const double2* tw = fftd::c_tw48;
+#pragma unroll
+    for (int m = 1; m < 16; m++) {
+      const double2 a = x[m + 15], v = x[m - 1];
+      double2 acc;
+      acc.x = fma(-0.5, v.x, a.x);
+      acc.x = fma(-sg, v.y, acc.x);
+      acc.y = fma(-0.5, v.y, a.y);
+      acc.y = fma(sg, v.x, acc.y);
+      u[m] = fftd::cmul_s<1>(tw[r * m], acc);
+    }
+  }
+  fftd::fft16<1>(u);
+}
+
+struct ZTask {
+  const double2* fh;   // staged f^ block [iz][j]
+  const double2* tb;   // staged table block [iz][j]
+  double2* W1b;        // W1 buffer of the term
+  int nh, h0, tau;     // staged pencils, first pencil, task (tau < nh: staged pencil, else its mirror)
+};
+// One Z pencil task: products, three output classes, stores.  Not inlined: one copy serves every call site
+// (prologue, R1, R2), which keeps the kernel's hot code small.
+__device__ __noinline__ void z_pencil(const ZTask z) {
+  const bool mir = z.tau >= z.nh;
+  const int j = mir ? z.tau - z.nh : z.tau;
+  double2 x[K];
+#pragma unroll
+  for (int i = 0; i < K; i++) {
+    const int ii = mir ? (K - 1 - i) : i;  // mirror (-lx,-ly): (a + ib)(l') conj(f^(l')) at reversed lz
+    const double2 f = z.fh[ii * z.nh + j], a = z.tb[ii * z.nh + j];
+    x[i] = mir ? make_double2(fma(a.x, f.x, a.y * f.y), fma(-a.x, f.y, a.y * f.x))
+               : make_double2(fma(a.x, f.x, -a.y * f.y), fma(a.x, f.y, a.y * f.x));
+  }
+  double2* W1b = z.W1b + (mir ? (NPEN - 1) - (z.h0 + j) : z.h0 + j);
+#pragma unroll 1
+  for (int r = 0; r < 3; r++) {
+    double2 u[16];
+    xform48_regs(x, r, u);
+#pragma unroll
+    for (int q = 0; q < 16; q++) W1b[(3 * q + r) * NPEN] = u[fftd::qslot(q)];
+  }
+}
+
+enum { TK_NONE = 0, TK_Y = 1, TK_X = 2, TK_Z = 3 };
+
+__global__ void __launch_bounds__(NTHR, 1) hot_kernel_v5(Args A) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ uint32_t tmem_base_sh;
+  __shared__ __align__(8) uint64_t bar_w1, bar_fh, bar_tab[2];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int team = blockIdx.x / TM, k = blockIdx.x - (blockIdx.x / TM) * TM;
+  constexpr int NLOW = NPEN / 2 + 1;
+  const int h0 = (k * NLOW) / TM, h1 = ((k + 1) * NLOW) / TM;
+  const int nh = h1 - h0;
+  const int nmir = (h1 == NLOW) ? nh - 1 : nh;
+  const int na = nh + nmir;
+  double2* W1t = A.W1 + (long long)team * NB * W1_BUF;
+  unsigned* zcnt = A.ctr + (long long)team * CTR_STRIDE;
+  unsigned* ycnt = zcnt + 32 * NB;
+  const long long ncell_team = (team < A.n_cells) ? (A.n_cells - 1 - team) / A.nteams + 1 : 0;
+  const long long TT = ncell_team * A.T1;  // terms of this team
+  double2* w1in = reinterpret_cast<double2*>(smem);
+  double2* ysh = reinterpret_cast<double2*>(smem + OFF_Y);
+  double2* fh = reinterpret_cast<double2*>(smem + OFF_FH);
+  double2* tbs = reinterpret_cast<double2*>(smem + OFF_TB);
+  const uint32_t zblk = (uint32_t)(K * nh) * 16u;
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;"
+                 ::"r"((uint32_t)__cvta_generic_to_shared(&tmem_base_sh)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    mbar_init(&bar_w1);
+    mbar_init(&bar_fh);
+    mbar_init(&bar_tab[0]);
+    mbar_init(&bar_tab[1]);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tbase = tmem_base_sh;
+  if (TT == 0) goto done;
+  {
+    auto cell_of = [&](long long tz) { return team + (tz / A.T1) * (long long)A.nteams; };
+    auto issue_tab = [&](long long tz) {  // table block of term tz into buffer tz % 2
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      uint64_t* b = &bar_tab[tz & 1];
+      mbar_expect(b, zblk);
+      bulk_g2s(tbs + (tz & 1) * (ZBLK_B / 16), A.tabT + (long long)(tz % A.T1) * LHN + K * h0, zblk, b);
+    };
+    auto issue_fh = [&](long long cell) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_expect(&bar_fh, zblk);
+      bulk_g2s(fh, A.fhatT + cell * (long long)LHN + K * h0, zblk, &bar_fh);
+    };
+    auto w1_ready = [&](long long tz) {
+      return ld_acquire(zcnt + 32 * (tz % NB)) >= (unsigned)(TM * (tz / NB + 1));
+    };
+    auto issue_w1 = [&](long long tz) {
+      const double2* src = W1t + (tz % NB) * (long long)W1_BUF + (long long)(PLN * k) * NPEN;
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_expect(&bar_w1, PLN * W1IN_B);
+      bulk_g2s(w1in, src, PLN * W1IN_B, &bar_w1);  // the member's 4 planes are contiguous
+    };
+    auto z_task = [&](long long tz, int tau) {
+      z_pencil(ZTask{fh, tbs + (tz & 1) * (ZBLK_B / 16), W1t + (tz % NB) * (long long)W1_BUF, nh, h0, tau});
+    };
+    auto publish_z = [&](long long tz) {
+      __threadfence();
+      atomicAdd(zcnt + 32 * (tz % NB), 1u);
+    };
+    auto wait_buffer_free = [&](long long tz) {  // all members consumed W1(tz - NB)
+      if (tz >= NB) poll_ge(ycnt + 32 * (tz % NB), (unsigned)(TM * (tz / NB)));
+    };
+
+    // ---------------- prologue: Z(0) complete, Z(1) part A ----------------
+    uint32_t par_fh = 0;
+    if (tid == 0) {
+      issue_fh(cell_of(0));
+      issue_tab(0);
+      if (TT > 1) issue_tab(1);
+    }
+    if (warp >= 4) {
+      mbar_wait(&bar_fh, par_fh);
+      mbar_wait(&bar_tab[0], 0);
+      const int tau = tid - 128;
+      if (tau < na) z_task(0, tau);
+    }
+    __syncthreads();
+    par_fh ^= 1;
+    if (tid == 0) {
+      publish_z(0);
+      if (TT > 2) issue_tab(2);  // buffer 0 is free again
+    }
+    if (TT > 1 && warp >= 6) {
+      const long long tz = 1;
+      if (tz % A.T1 == 0) {  // new cell (T1 == 1 only)
+        if (tid == 192) issue_fh(cell_of(tz));
+        mbar_wait(&bar_fh, par_fh);
+      }
+      mbar_wait(&bar_tab[1], 0);
+      const int tau = tid - 192;
+      if (tau < ZA && tau < na) z_task(tz, tau);
+    }
+    if (TT > 1 && A.T1 == 1) par_fh ^= 1;
+    __syncthreads();
+
+    const bool leader = (tid == 0);
+    bool w1_issued = false;
+    uint32_t par_w1 = 0;
+    const int xw = warp;                                  // X warps 0..5: rows 32 xw + lane
+    const uint32_t tG = tbase + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(96 * (warp >> 2));
+#pragma unroll 1
+    for (long long tg = 0; tg < TT; tg++) {
+      const int t = (int)(tg % A.T1);
+      const long long cell = cell_of(tg);
+      long long* st = (A.dbg && leader && tg >= 2 && tg < 6) ? A.dbg + (long long)blockIdx.x * 128 + (tg - 2) * 16 : nullptr;
+      if (st) st[0] = clock64();
+      // ---- W1(tg) in shared memory ----
+      if (leader) {
+        if (!w1_issued) {
+          poll_ge(zcnt + 32 * (tg % NB), (unsigned)(TM * (tg / NB + 1)));
+          issue_w1(tg);
+        }
+        w1_issued = false;
+      }
+      if (warp < 4) mbar_wait(&bar_w1, par_w1);
+      par_w1 ^= 1;
+      if (st) st[1] = clock64();
+      if (leader) {
+        __threadfence();
+        atomicAdd(ycnt + 32 * (tg % NB), 1u);  // W1(tg) consumed by this member
+      }
+      // ---- R1: Y(tg) on warps 0-3, Z(tg+1) part B on warp 4 ----
+      {
+        int kind = TK_NONE;
+        if (warp < 4 && lane < K) kind = TK_Y;
+        else if (warp == 4 && tg + 1 < TT && ZA + lane < na) kind = TK_Z;
+        if (kind == TK_Y) {
+          const double2* src = w1in + warp * NPEN + lane * K;  // pencil lx = lane of plane w
+          double2 x[K];
+#pragma unroll
+          for (int i = 0; i < K; i++) x[i] = src[i];
+          double2* dst = ysh + warp * YPL + lane;             // Y[p][py][ix]
+#pragma unroll 1
+          for (int r = 0; r < 3; r++) {
+            double2 u[16];
+            xform48_regs(x, r, u);
+#pragma unroll
+            for (int q = 0; q < 16; q++) dst[(3 * q + r) * K] = u[fftd::qslot(q)];
+          }
+        } else if (kind == TK_Z) {
+          z_task(tg + 1, ZA + lane);
+        }
+      }
+      __syncthreads();
+      if (st) st[2] = clock64();
+      if (tid == 128 && tg + 1 < TT) publish_z(tg + 1);  // Z(tg+1) complete in this member
+      if (tid == 192 && tg + 3 < TT) issue_tab(tg + 3);  // buffer (tg+1) % 2 is free
+      // f^ of the next cell: last used by Z(tg+1) part B (this R1); first needed by Z(tg+2) part A (R2)
+      const bool new_cell_z = (tg + 2 < TT) && ((tg + 2) % A.T1 == 0);
+      if (new_cell_z && tid == 192) issue_fh(cell_of(tg + 2));
+      if (leader && tg + 1 < TT && w1_ready(tg + 1)) {  // input planes are free: copy during R2
+        issue_w1(tg + 1);
+        w1_issued = true;
+      }
+      // ---- R2: X(tg) on warps 0-5, Z(tg+2) part A on warps 6-7 ----
+      if (warp < 6) {
+        if (t == 0) {  // zero this warp's G accumulators
+          uint32_t zw[32];
+#pragma unroll
+          for (int i = 0; i < 32; i++) zw[i] = 0u;
+#pragma unroll
+          for (int c = 0; c < 3; c++) tmem_st32(tG + 32 * c, zw);
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        }
+        const int rho = 32 * xw + lane, pl = rho / P, py = rho - (rho / P) * P;
+        const double2* src = ysh + pl * YPL + py * K;
+        double2 x[K];
+#pragma unroll
+        for (int i = 0; i < K; i++) x[i] = src[i];
+#pragma unroll 1
+        for (int r = 0; r < 3; r++) {
+          double2 u[16];
+          xform48_regs(x, r, u);
+#pragma unroll
+          for (int hh = 0; hh < 2; hh++) {
+            uint32_t gw[16];
+            tmem_ld16(tG + 32 * r + 16 * hh, gw);
+#pragma unroll
+            for (int q = 0; q < 8; q++) {
+              const double2 z = u[fftd::qslot(8 * hh + q)];
+              const double acc = fma(z.x, z.y, __hiloint2double((int)gw[2 * q + 1], (int)gw[2 * q]));
+              gw[2 * q] = (uint32_t)__double2loint(acc);
+              gw[2 * q + 1] = (uint32_t)__double2hiint(acc);
+            }
+            tmem_st16(tG + 32 * r + 16 * hh, gw);
+          }
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        if (t == A.T1 - 1) {  // G[cell][px = 3q + r][pz][py]
+          double* Gc = A.G + cell * (long long)(P * P * P) + (long long)(PLN * k + pl) * P + py;
+#pragma unroll 1
+          for (int r = 0; r < 3; r++) {
+            uint32_t gw[32];
+            tmem_ld32(tG + 32 * r, gw);
+#pragma unroll
+            for (int q = 0; q < 16; q++)
+              Gc[(long long)(3 * q + r) * P * P] = __hiloint2double((int)gw[2 * q + 1], (int)gw[2 * q]);
+          }
+        }
+      } else if (tg + 2 < TT) {
+        const long long tz = tg + 2;
+        if (lane == 0) wait_buffer_free(tz);
+        __syncwarp();
+        if (tz % A.T1 == 0) {
+          mbar_wait(&bar_fh, par_fh);
+        }
+        mbar_wait(&bar_tab[tz & 1], (uint32_t)((tz >> 1) & 1));
+        const int tau = tid - 192;
+        if (tau < na) z_task(tz, tau);
+      }
+      if (new_cell_z) par_fh ^= 1;
+      __syncthreads();
+      if (st) st[3] = clock64();
+    }
+  }
+done:
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tbase));
+}
+}  // namespace v5
 
 }  // namespace f32
 
@@ -646,6 +1336,7 @@ fks_status fast_prepare(Ctx& c) {
   }
   cudaError_t e = cudaMemcpyToSymbol(c_w48, w, sizeof(w));
   if (e == cudaSuccess) e = xform32_prepare();
+  if (e == cudaSuccess) e = fftd::fill_twiddles();
   if (e != cudaSuccess) return cuda_status(e, "fast constants");
   e = cudaFuncSetAttribute(hot_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, R_BYTES);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(t12::hot_kernel_t12, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * t12::R_BYTES);
@@ -663,11 +1354,37 @@ fks_status fast_prepare(Ctx& c) {
             per_sm, (int)e, fa.numRegs, fa.sharedSizeBytes, t12::R_BYTES, fa.maxThreadsPerBlock);
 
   }
+  // variant: FKS_HOT = v4 (default: decoupled warp roles, one CTA per SM), t12 (two virtual CTAs per SM) or c6
+  // (6-CTA clusters)
   const char* hv = std::getenv("FKS_HOT");
-  const bool want_c6 = hv && std::string(hv) == "c6";
-  c.fast_variant = (!want_c6 && per_sm >= 1) ? t12::TM : CL;
+  const std::string want = hv ? std::string(hv) : std::string("v4");
+  int v4_per_sm = 0;
+  e = cudaFuncSetAttribute(v4::hot_kernel_v4, cudaFuncAttributeMaxDynamicSharedMemorySize, v4::SMEM_B);
+  if (e == cudaSuccess)
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v4_per_sm, v4::hot_kernel_v4, v4::NTHR, v4::SMEM_B);
+  if (e != cudaSuccess) { cudaGetLastError(); v4_per_sm = 0; }
+  int v5_per_sm = 0;
+  e = cudaFuncSetAttribute(v5::hot_kernel_v5, cudaFuncAttributeMaxDynamicSharedMemorySize, v5::SMEM_B);
+  if (e == cudaSuccess)
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v5_per_sm, v5::hot_kernel_v5, v5::NTHR, v5::SMEM_B);
+  if (e != cudaSuccess) { cudaGetLastError(); v5_per_sm = 0; }
+  if (want == "v5" && v5_per_sm >= 1) c.fast_kernel = 5;
+  else if (want == "v4" && v4_per_sm >= 1) c.fast_kernel = 4;
+  else if (want != "c6" && per_sm >= 1) c.fast_kernel = 3;
+  else c.fast_kernel = 2;
+  c.fast_variant = (c.fast_kernel == 2) ? CL : t12::TM;
   size_t w1_elems;
-  if (c.fast_variant == t12::TM) {
+  if (c.fast_kernel == 5) {
+    c.fast_nteams = c.num_sms / v5::TM;
+    w1_elems = (size_t)c.fast_nteams * v5::NB * W1_BUF;
+    e = cudaMalloc(&c.d_ctr, (size_t)c.fast_nteams * v5::CTR_STRIDE * sizeof(unsigned));
+    if (e != cudaSuccess) { cudaGetLastError(); return cuda_status(e, "team counters"); }
+  } else if (c.fast_kernel == 4) {
+    c.fast_nteams = c.num_sms / v4::TM;
+    w1_elems = (size_t)c.fast_nteams * v4::NB * W1_BUF;
+    e = cudaMalloc(&c.d_ctr, (size_t)c.fast_nteams * v4::CTR_STRIDE * sizeof(unsigned));
+    if (e != cudaSuccess) { cudaGetLastError(); return cuda_status(e, "team counters"); }
+  } else if (c.fast_kernel == 3) {
     c.fast_nteams = (2 * c.num_sms) / t12::TM;  // two virtual CTAs (warp groups) per SM
     w1_elems = (size_t)c.fast_nteams * 2 * W1_BUF;
     e = cudaMalloc(&c.d_ctr, (size_t)c.fast_nteams * 32 * sizeof(unsigned));
@@ -705,7 +1422,23 @@ fks_status fast_collision(Ctx& c, const double* fin, double* out, long long n, b
   c.prof.end(1, st);
 
   c.prof.begin(2, st);
-  if (c.fast_variant == t12::TM) {
+  if (c.fast_kernel == 5) {
+    const long long nt = std::min<long long>(c.fast_nteams, n);
+    v5::Args A{fhT, c.d_abT, G, c.d_w1, c.d_ctr, n, c.T + 1, (int)nt, c.dbg};
+    cudaMemsetAsync(c.d_ctr, 0, (size_t)c.fast_nteams * v5::CTR_STRIDE * sizeof(unsigned), st);
+    void* args[] = {&A};
+    cudaError_t e = cudaLaunchCooperativeKernel((void*)v5::hot_kernel_v5, dim3((unsigned)(nt * v5::TM)),
+                                                dim3(v5::NTHR), args, v5::SMEM_B, st);
+    if (e != cudaSuccess) { c.prof.end(2, st); return cuda_status(e, "cooperative hot kernel launch (v5)"); }
+  } else if (c.fast_kernel == 4) {
+    const long long nt = std::min<long long>(c.fast_nteams, n);
+    v4::Args A{fhT, c.d_abT, G, c.d_w1, c.d_ctr, n, c.T + 1, (int)nt, c.dbg};
+    cudaMemsetAsync(c.d_ctr, 0, (size_t)c.fast_nteams * v4::CTR_STRIDE * sizeof(unsigned), st);
+    void* args[] = {&A};
+    cudaError_t e = cudaLaunchCooperativeKernel((void*)v4::hot_kernel_v4, dim3((unsigned)(nt * v4::TM)),
+                                                dim3(v4::NTHR), args, v4::SMEM_B, st);
+    if (e != cudaSuccess) { c.prof.end(2, st); return cuda_status(e, "cooperative hot kernel launch (v4)"); }
+  } else if (c.fast_kernel == 3) {
     const char* ps = std::getenv("FKS_PHASE_SHIFT");
     t12::Args A{fhT, c.d_abT, G, c.d_w1, c.d_ctr, n, c.T + 1, c.dbg, ps ? std::atoll(ps) : 15000LL};
     // teams are formed from the 2 * grid virtual CTAs; keep an even team count so both warp groups have work

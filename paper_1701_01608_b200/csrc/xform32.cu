@@ -7,9 +7,11 @@
 //
 //   forward  Kf1 plane jx : f(jx,jy,jz)  --z (real, lz=0..15)--> --y (ly in K')-->  F2[cell][jx][ly][lz]
 //            Kf2 column ly: F2(:,ly,lz)  --x (lx in K'), N^-3-->  f^T[cell][lz][lx*31+ly] and its conjugate at -l
-//   back     Kb1 plane px : G(px,py,pz)  --z (real, kz=0..15)--> --y (ky in K')--> H2[cell][px][ky][kz]
-//            Kb2 column ky: H2(:,ky,kz)  --x (kx in K'), P^-3, [Q^_0 := 0]--> --x inverse (jx)--> E1[cell][jx][ky][kz]
-//            Kb3 plane jx : E1(jx,:,:)   --y inverse (jy)--> --z Hermitian->real (jz)-->  Q (or f* + s Q)
+//   back     Kb1 plane px : G[cell][px][pz][py] --y (real, ky=0..15)--> --z (kz in K')--> H2[cell][px][kz][ky]
+//            Kb2 column kz: H2(:,kz,ky)  --x (kx in K'), P^-3, [Q^_0 := 0]--> --x inverse (jx)--> E1[cell][jx][kz][ky]
+//            Kb3 plane jx : E1(jx,:,:)   --z inverse (jz)--> --y Hermitian->real (jy)-->  Q (or f* + s Q)
+// (G is stored py-fastest so that the term-loop kernel writes it coalesced; the real axis of the back transform
+// is therefore y.  Inside kb1..kb3 the loop variables keep the generic names "row"/"col".)
 #include <algorithm>
 #include "fks_internal.cuh"
 #include "fft_dev.cuh"
@@ -139,12 +141,13 @@ __global__ void __launch_bounds__(256) kf2(const double2* __restrict__ F2, doubl
 }
 
 // ---- back ---------------------------------------------------------------------------------------------
-// kb1: CTA = (cell, 4 px planes), 288 threads.  z: two real rows packed as one complex row, FFT48, untangled
-// on the fly by the y tasks (kz = 0..15);  y: FFT48 over py -> ky in K'.  Out H2[cell][px][ky][kz].
+// kb1: CTA = (cell, 4 px planes), 288 threads.  First axis (py, contiguous): two real rows packed as one
+// complex row, FFT48, untangled on the fly (ky = 0..15);  second axis (pz): FFT48 -> kz in K'.
+// Out H2[cell][px][kz][ky].
 __global__ void __launch_bounds__(288) kb1(const double* __restrict__ G, double2* __restrict__ H2) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  // [4 planes][24 row pairs][ZS]: element pz of the pair = (G(2pr, pz), G(2pr+1, pz)); then in place the
-  // complex FFT48 of the pair
+  // [4 planes][24 row pairs][ZS]: element py of the pair = (G(pz = 2pr, py), G(pz = 2pr+1, py)); then in
+  // place the complex FFT48 of the pair
   double2* zc = reinterpret_cast<double2*>(smem_raw);
   const int tid = threadIdx.x;
   const long long cell = blockIdx.x / (P / PB1);
@@ -154,8 +157,8 @@ __global__ void __launch_bounds__(288) kb1(const double* __restrict__ G, double2
     double* dst = reinterpret_cast<double*>(zc);
 #pragma unroll 4
     for (int i = tid; i < PB1 * P * P; i += 288) {
-      const int row = i / P, pz = i - row * P;  // row = s * 48 + py
-      dst[((row >> 1) * ZS + pz) * 2 + (row & 1)] = src[i];
+      const int row = i / P, col = i - row * P;  // row = s * 48 + pz, col = py
+      dst[((row >> 1) * ZS + col) * 2 + (row & 1)] = src[i];
     }
   }
   __syncthreads();
@@ -253,8 +256,8 @@ __global__ void __launch_bounds__(192) kb2(const double2* __restrict__ H2, doubl
   }
 }
 
-// kb3: CTA = (cell, 8 jx planes).  y: inverse FFT32 over ky -> jy;  z: Hermitian -> real inverse FFT32 (packed
-// FFT16); then Q or f* + s Q with coalesced stores.
+// kb3: CTA = (cell, 8 jx planes).  z: inverse FFT32 over kz -> jz;  y: Hermitian -> real inverse FFT32 (packed
+// FFT16); then Q or f* + s Q, transposed through shared memory into coalesced stores.
 __global__ void __launch_bounds__(256) kb3(const double2* __restrict__ E1, const double* fin, double* out,
                                            int euler, double s) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -301,17 +304,15 @@ __global__ void __launch_bounds__(256) kb3(const double2* __restrict__ E1, const
     for (int n = 0; n < 16; n++) row[n] = u[qslot(n)];  // (x[2n], x[2n+1])
   }
   __syncthreads();
+  // buf row (plane, jz) holds (Q(jy = 2n, jz), Q(jy = 2n+1, jz)) at element n: transpose while storing
   const long long base = (cell * N + jx0) * N * N;
-  const double2* fi = reinterpret_cast<const double2*>(fin + base);
-  double2* o = reinterpret_cast<double2*>(out + base);
+  const double* bd = reinterpret_cast<const double*>(buf);
 #pragma unroll 4
-  for (int i = tid; i < PL8 * N * H; i += 256) {
-    double2 v = buf[(i >> 4) * RS + (i & 15)];
-    if (euler) {
-      const double2 a = fi[i];
-      v = make_double2(fma(s, v.x, a.x), fma(s, v.y, a.y));
-    }
-    o[i] = v;
+  for (int i = tid; i < PL8 * N * N; i += 256) {
+    const int pl = i >> 10, jy = (i >> 5) & 31, jz = i & 31;
+    double v = bd[((pl * N + jz) * RS + (jy >> 1)) * 2 + (jy & 1)];
+    if (euler) v = fma(s, v, fin[base + i]);
+    out[base + i] = v;
   }
 }
 
