@@ -29,7 +29,8 @@ def up_to_date() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
         return LIB
-    cmd = [NVCC] + FLAGS + sources() + ["-o", LIB]
+    extra = os.environ.get("FKS_NVCC_EXTRA", "").split()
+    cmd = [NVCC] + FLAGS + extra + sources() + ["-o", LIB]
     r = subprocess.run(cmd, capture_output=True, text=True)
     log = os.path.join(HERE, "build.log")
     with open(log, "w") as fh:

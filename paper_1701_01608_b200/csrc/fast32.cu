@@ -112,14 +112,16 @@ __device__ __forceinline__ void mbar_expect(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(bar)),
                "r"(bytes) : "memory");
 }
+// Waiting warps are suspended by the hardware (try_wait with a suspend-time hint) instead of spinning: spinning
+// waiters cost ~14 % of the issue slots of the working warps sharing their sub-partition (ncu, hot kernel v4).
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t a = (uint32_t)__cvta_generic_to_shared(bar);
   uint32_t done = 0;
   long long spins = 0;
   while (!done) {
-    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-                 : "=r"(done) : "r"(a), "r"(parity) : "memory");
-    if (++spins > (1LL << 28)) asm volatile("trap;");  // never hang the GPU on a byte-count bug
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(done) : "r"(a), "r"(parity), "r"(1000000u) : "memory");
+    if (++spins > (1LL << 24)) asm volatile("trap;");  // never hang the GPU on a byte-count bug
   }
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -643,8 +645,11 @@ __global__ void __launch_bounds__(2 * NT, 1) hot_kernel_t12(Args A) {
 namespace v4 {
 constexpr int TM = 12;                        // CTAs (members) per team = per cell
 constexpr int PLN = P / TM;                   // 4 z-planes per member
-constexpr int NB = 3;                         // W1 team buffers (Z warps run ahead by < NB terms)
-constexpr int NYX = 6, NZW = 2;               // YX warps (2 groups of 3), Z warps (3 Z warps cap registers at 168)
+constexpr int NB = 4;                         // W1 team buffers (Z warps run ahead by < NB terms)
+#ifndef V4_NZW
+#define V4_NZW 2
+#endif
+constexpr int NYX = 6, NZW = V4_NZW;          // YX warps (2 groups of 3), Z warps (3+ Z warps cap registers at 168)
 constexpr int NTHR = 32 * (NYX + NZW);        // 288
 constexpr int NZT = 32 * NZW;                 // Z threads
 constexpr int MAXH = 41;                      // max staged pencils per member (481 / 12 rounded up)
@@ -681,6 +686,7 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
 __device__ __forceinline__ void poll_ge(const unsigned* p, unsigned target) {
   long long spins = 0;
   while (ld_acquire(p) < target) {
+    __nanosleep(128);
     if (++spins > (1LL << 25)) asm volatile("trap;");  // never hang the GPU on a counting bug
   }
 }
@@ -741,6 +747,49 @@ __device__ __forceinline__ void xform48(const double2* base, int ld, int r, doub
     }
   }
   fftd::fft16<1>(u);
+}
+
+// Two independent class-r transforms interleaved (ILP 2) for the fused R4+R5 X round.
+__device__ __forceinline__ void xform48x2(const double2* b1, const double2* b2, int r, double2 (&u)[16],
+                                          double2 (&v)[16]) {
+  u[0] = b1[15];
+  v[0] = b2[15];
+  if (r == 0) {
+#pragma unroll
+    for (int m = 1; m < 16; m++) {
+      u[m] = fftd::cadd(b1[m + 15], b1[m - 1]);
+      v[m] = fftd::cadd(b2[m + 15], b2[m - 1]);
+    }
+  } else {
+    const double sg = (r == 1) ? -0.86602540378443864676 : 0.86602540378443864676;
+#pragma unroll
+    for (int m = 1; m < 16; m++) {
+      const double2 w = fftd::c_tw48[r * m];
+      const double2 a1 = b1[m + 15], c1 = b1[m - 1], a2 = b2[m + 15], c2 = b2[m - 1];
+      double2 s1, s2;
+      s1.x = fma(-0.5, c1.x, a1.x); s2.x = fma(-0.5, c2.x, a2.x);
+      s1.x = fma(-sg, c1.y, s1.x);  s2.x = fma(-sg, c2.y, s2.x);
+      s1.y = fma(-0.5, c1.y, a1.y); s2.y = fma(-0.5, c2.y, a2.y);
+      s1.y = fma(sg, c1.x, s1.y);   s2.y = fma(sg, c2.x, s2.y);
+      u[m] = fftd::cmul_s<1>(w, s1);
+      v[m] = fftd::cmul_s<1>(w, s2);
+    }
+  }
+  fftd::fft16<1>(u);
+  fftd::fft16<1>(v);
+}
+
+__device__ __forceinline__ void g_accumulate(uint32_t tcol, const double2 (&u)[16]) {
+  uint32_t gw[32];
+  tmem_ld32(tcol, gw);
+#pragma unroll
+  for (int q = 0; q < 16; q++) {
+    const double2 z = u[fftd::qslot(q)];
+    const double acc = fma(z.x, z.y, __hiloint2double((int)gw[2 * q + 1], (int)gw[2 * q]));
+    gw[2 * q] = (uint32_t)__double2loint(acc);
+    gw[2 * q + 1] = (uint32_t)__double2hiint(acc);
+  }
+  tmem_st32(tcol, gw);
 }
 
 __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
@@ -829,18 +878,27 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         }
 #pragma unroll 1
-        for (int rd = 0; rd < 5; rd++) {
-          // task of this warp in round rd (see the schedule above)
-          const bool isx = (rd == 1 || rd == 3 || rd == 4);
+        for (int rd = 0; rd < 4; rd++) {
+          // task of this warp in round rd (see the schedule above; rd == 3 fuses R4 and R5)
+          if (rd == 3) {
+            double2 u[16], v[16];
+            xform48x2(ybuf(xp, 1) + xq * K, ybuf(xp, 0) + xq * K, wr, u, v);
+            g_accumulate(tG + 32u, u);
+            g_accumulate(tG + 64u, v);
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            nbar(1 + g, 96);
+            if (st) st[5] = clock64();
+            break;
+          }
+          const bool isx = (rd == 1);
           const double2* base;
           double2* ydst = nullptr;
           int r;
           uint32_t tcol = 0;
           if (isx) {
-            const int slot = (rd == 3) ? 1 : 0;
-            base = ybuf(xp, slot) + xq * K;
+            base = ybuf(xp, 0) + xq * K;
             r = wr;
-            tcol = tG + (rd == 1 ? 0u : (rd == 3 ? 32u : 64u));
+            tcol = tG;
           } else {
             // R1: (p0,c0) (p1,c0) (p0,c1);  R3: (p1,c1) (p0,c2) (p1,c2)
             const int code = (rd == 0) ? wr : 3 + wr;
@@ -853,24 +911,13 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
           double2 u[16];
           xform48(base, 1, r, u);
           if (isx) {  // G(px = 3q + r, row) += Re z * Im z
-            uint32_t gw[32];
-            tmem_ld32(tcol, gw);
-#pragma unroll
-            for (int q = 0; q < 16; q++) {
-              const double2 z = u[fftd::qslot(q)];
-              const double acc = fma(z.x, z.y, __hiloint2double((int)gw[2 * q + 1], (int)gw[2 * q]));
-              gw[2 * q] = (uint32_t)__double2loint(acc);
-              gw[2 * q + 1] = (uint32_t)__double2hiint(acc);
-            }
-            tmem_st32(tcol, gw);
+            g_accumulate(tcol, u);
           } else if (lane < K) {
 #pragma unroll
             for (int q = 0; q < 16; q++) ydst[q * K] = u[fftd::qslot(q)];
           }
-          if (rd == 3) continue;  // R4 -> R5: both only read
-          if (rd == 4) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
           nbar(1 + g, 96);
-          if (st) st[2 + (rd == 0 ? 0 : rd == 1 ? 1 : rd == 2 ? 2 : 3)] = clock64();
+          if (st) st[2 + rd] = clock64();
           if (rd == 2 && leader && tg + 1 < total_tg &&
               ld_acquire(zcnt + 32 * ((tg + 1) % NB)) >= (unsigned)(TM * ((tg + 1) / NB + 1))) {
             issue_w1(tg + 1);  // input planes are free: overlap the copy with R4/R5
@@ -928,19 +975,17 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
         if (st) st[1] = clock64();
         // products: Z = (a + ib) f^ for the staged pencils, and for their mirrors (-lx,-ly): (a + ib) conj(f^)
         // at the reversed lz (a, b even; f real)
-        {  // element pairs {i, 30 - i} of pencil j, e = i * nh + j, walked without division
-          int i = zt / nh, j = zt - (zt / nh) * nh;
-#pragma unroll 2
+        {  // element pairs {i, 30 - i} of pencil j, e = i * nh + j; i = e / nh by multiply-high (exact: e nh < 2^32)
+          const unsigned mdiv = 0xffffffffu / (unsigned)nh + 1u;
+#pragma unroll 4
           for (int e = zt; e < 16 * nh; e += NZT) {
-            const int i2 = 30 - i;
+            const int i = (int)__umulhi((unsigned)e, mdiv), j = e - i * nh, i2 = 30 - i;
             const double2 f1 = fh[i * nh + j], a1 = tb[i * nh + j];
             const double2 f2 = fh[i2 * nh + j], a2 = tb[i2 * nh + j];
             zp[i * nh + j] = make_double2(fma(a1.x, f1.x, -a1.y * f1.y), fma(a1.x, f1.y, a1.y * f1.x));
             zp[i2 * nh + j] = make_double2(fma(a2.x, f2.x, -a2.y * f2.y), fma(a2.x, f2.y, a2.y * f2.x));
             zm[i * nh + j] = make_double2(fma(a2.x, f2.x, a2.y * f2.y), fma(-a2.x, f2.y, a2.y * f2.x));
             zm[i2 * nh + j] = make_double2(fma(a1.x, f1.x, a1.y * f1.y), fma(-a1.x, f1.y, a1.y * f1.x));
-            j += NZT;
-            while (j >= nh) { j -= nh; i++; }
           }
         }
         nbar(3, NZT);  // products complete; tb (and, after the last term, fh) free

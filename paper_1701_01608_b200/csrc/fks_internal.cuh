@@ -42,6 +42,8 @@ struct Ctx {
   int fast_ncl = 0;                     // fast path: co-resident clusters (persistent grid)
   double2* d_w1 = nullptr;
   long long* dbg = nullptr;
+  long long* prog_host = nullptr;       // debug: mapped pinned per-warp progress words (FKS_DEBUG_PROGRESS)
+  long long* prog_dev = nullptr;
   int fast_kernel = 0;                  // fast path term-loop kernel: 2 = 6-CTA clusters, 3 = t12, 4 = v4
   int fast_variant = 6;                 // fast path: CTAs per cell (6 = cluster kernel, 12 = two-CTAs-per-SM teams)
   int fast_nteams = 0;                  // fast path (variant 12): co-resident teams

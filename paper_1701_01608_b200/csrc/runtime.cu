@@ -236,6 +236,17 @@ fks_status fks_collision_init_ex(fks_ctx** out, const fks_params* pp) {
     rc = fast_prepare(*c);
     if (rc) { fks_destroy(reinterpret_cast<fks_ctx*>(c)); return rc; }
   }
+  if (std::getenv("FKS_DEBUG_PROGRESS")) {  // mapped host memory the device writes while running (hang probes)
+    void* hp = nullptr;
+    if (cudaHostAlloc(&hp, 4096 * 16 * sizeof(long long), cudaHostAllocMapped) == cudaSuccess) {
+      std::memset(hp, 0, 4096 * 16 * sizeof(long long));
+      c->prog_host = (long long*)hp;
+      void* dp = nullptr;
+      if (cudaHostGetDevicePointer(&dp, hp, 0) == cudaSuccess) c->prog_dev = (long long*)dp;
+    } else {
+      cudaGetLastError();
+    }
+  }
   if (std::getenv("FKS_PHASE_TIMING")) {  // debug instrumentation of the hot kernel (tools/phase_timing.py)
     if (cudaMalloc(&c->dbg, 64 * 1024 * sizeof(long long)) == cudaSuccess) cudaMemset(c->dbg, 0, 64 * 1024 * sizeof(long long));
     else { cudaGetLastError(); c->dbg = nullptr; }
@@ -443,6 +454,11 @@ long long fks_debug_timestamps(const fks_ctx* h, long long* host, long long n) {
   return n;
 }
 
+// debug only (not in fks.h): host address of the mapped progress words, 0 if disabled
+extern "C" long long fks_debug_progress_ptr(const fks_ctx* h) {
+  return h ? (long long)reinterpret_cast<const Ctx*>(h)->prog_host : 0;
+}
+
 long long fks_launch_count(const fks_ctx* h) {
   return h ? reinterpret_cast<const Ctx*>(h)->launches : -1;
 }
@@ -461,6 +477,7 @@ void fks_destroy(fks_ctx* h) {
   if (c->d_abT) cudaFree(c->d_abT);
   if (c->d_w1) cudaFree(c->d_w1);
   if (c->dbg) cudaFree(c->dbg);
+  if (c->prog_host) cudaFreeHost(c->prog_host);
   if (c->d_ctr) cudaFree(c->d_ctr);
   if (c->d_twN) cudaFree(c->d_twN);
   if (c->d_twP) cudaFree(c->d_twP);
