@@ -975,17 +975,36 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
         if (st) st[1] = clock64();
         // products: Z = (a + ib) f^ for the staged pencils, and for their mirrors (-lx,-ly): (a + ib) conj(f^)
         // at the reversed lz (a, b even; f real)
-        {  // element pairs {i, 30 - i} of pencil j, e = i * nh + j; i = e / nh by multiply-high (exact: e nh < 2^32)
+        {  // element pairs {i, 30 - i} of pencil j, e = i * nh + j; i = e / nh by multiply-high (exact: e nh < 2^32).
+           // Four iterations are loaded before any store (the product buffers never alias the staged inputs).
           const unsigned mdiv = 0xffffffffu / (unsigned)nh + 1u;
-#pragma unroll 4
-          for (int e = zt; e < 16 * nh; e += NZT) {
-            const int i = (int)__umulhi((unsigned)e, mdiv), j = e - i * nh, i2 = 30 - i;
-            const double2 f1 = fh[i * nh + j], a1 = tb[i * nh + j];
-            const double2 f2 = fh[i2 * nh + j], a2 = tb[i2 * nh + j];
-            zp[i * nh + j] = make_double2(fma(a1.x, f1.x, -a1.y * f1.y), fma(a1.x, f1.y, a1.y * f1.x));
-            zp[i2 * nh + j] = make_double2(fma(a2.x, f2.x, -a2.y * f2.y), fma(a2.x, f2.y, a2.y * f2.x));
-            zm[i * nh + j] = make_double2(fma(a2.x, f2.x, a2.y * f2.y), fma(-a2.x, f2.y, a2.y * f2.x));
-            zm[i2 * nh + j] = make_double2(fma(a1.x, f1.x, a1.y * f1.y), fma(-a1.x, f1.y, a1.y * f1.x));
+          const double2* __restrict__ fr = fh;
+          const double2* __restrict__ tr = tb;
+          double2* __restrict__ pw = zp;
+          double2* __restrict__ mw = zm;
+          const int ne = 16 * nh;
+#pragma unroll 1
+          for (int e0 = zt; e0 < ne; e0 += 4 * NZT) {
+            double2 f1[4], a1[4], f2[4], a2[4];
+            int o1[4], o2[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+              const int e = min(e0 + u * NZT, ne - 1);
+              const int i = (int)__umulhi((unsigned)e, mdiv), j = e - i * nh;
+              o1[u] = i * nh + j;
+              o2[u] = (30 - i) * nh + j;
+              f1[u] = fr[o1[u]]; a1[u] = tr[o1[u]];
+              f2[u] = fr[o2[u]]; a2[u] = tr[o2[u]];
+            }
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+              if (e0 + u * NZT < ne) {
+                pw[o1[u]] = make_double2(fma(a1[u].x, f1[u].x, -a1[u].y * f1[u].y), fma(a1[u].x, f1[u].y, a1[u].y * f1[u].x));
+                pw[o2[u]] = make_double2(fma(a2[u].x, f2[u].x, -a2[u].y * f2[u].y), fma(a2[u].x, f2[u].y, a2[u].y * f2[u].x));
+                mw[o1[u]] = make_double2(fma(a2[u].x, f2[u].x, a2[u].y * f2[u].y), fma(-a2[u].x, f2[u].y, a2[u].y * f2[u].x));
+                mw[o2[u]] = make_double2(fma(a1[u].x, f1[u].x, a1[u].y * f1[u].y), fma(-a1[u].x, f1[u].y, a1[u].y * f1[u].x));
+              }
+            }
           }
         }
         nbar(3, NZT);  // products complete; tb (and, after the last term, fh) free
