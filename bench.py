@@ -240,6 +240,16 @@ def main():
     achieved = fl["hot"] * cells_per_launch / (hot_ms / 1e3) / 1e12
     peak = fp64_peak_tflops(1965.0)
     clocks = clk.summary()
+    # DRAM traffic of the dominant kernel from the committed ncu --set full capture (per cell, scaled to this
+    # run's cells per launch); null when no capture of the current kernel is committed
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "r01g_hot_kernel_traffic.json")
+    if os.path.exists(tpath) and col.info.get("path") == 2:
+        try:
+            tj = json.load(open(tpath))
+            traffic = tj["dram_bytes_per_cell"] * cells_per_launch
+        except Exception:
+            traffic = None
 
     # end to end through the host-buffer C-ABI call (pinned host memory, copies inside the timed region)
     e2e = None
@@ -271,7 +281,9 @@ def main():
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": workload,
         "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": achieved / peak, "traffic": None,
+                     "frac": achieved / peak, "traffic": traffic,
+                     "traffic_note": "dram__bytes_read+write per launch from profiles/r01g_hot_kernel_traffic.json "
+                                     "(ncu --set full of this kernel in this bench command), scaled to cells per launch",
                      "kernel": "term loop (a3-a5: table product, pruned 3D inverse, gain-loss accumulate)",
                      "flop_per_cell": fl["hot"], "cells_per_launch": cells_per_launch, "ms_per_launch": hot_ms,
                      "peak_note": "FP64 DFMA: 148 SM x 64 lanes x 2 flop x 1965 MHz (unit counts, max clock); "
