@@ -690,6 +690,11 @@ __device__ __forceinline__ void poll_ge(const unsigned* p, unsigned target) {
     if (++spins > (1LL << 25)) asm volatile("trap;");  // never hang the GPU on a counting bug
   }
 }
+// publication of W1 by one thread after a named barrier: release semantics are cumulative over the stores the
+// barrier made visible to it (a separate fence.sc cost ~1.3 K cycles per term)
+__device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ void nbar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
 __device__ __forceinline__ void tmem_ld32(uint32_t addr, uint32_t (&v)[32]) {
@@ -766,6 +771,36 @@ __device__ __forceinline__ void xform48x2(const double2* b1, const double2* b2, 
     for (int m = 1; m < 16; m++) {
       const double2 w = fftd::c_tw48[r * m];
       const double2 a1 = b1[m + 15], c1 = b1[m - 1], a2 = b2[m + 15], c2 = b2[m - 1];
+      double2 s1, s2;
+      s1.x = fma(-0.5, c1.x, a1.x); s2.x = fma(-0.5, c2.x, a2.x);
+      s1.x = fma(-sg, c1.y, s1.x);  s2.x = fma(-sg, c2.y, s2.x);
+      s1.y = fma(-0.5, c1.y, a1.y); s2.y = fma(-0.5, c2.y, a2.y);
+      s1.y = fma(sg, c1.x, s1.y);   s2.y = fma(sg, c2.x, s2.y);
+      u[m] = fftd::cmul_s<1>(w, s1);
+      v[m] = fftd::cmul_s<1>(w, s2);
+    }
+  }
+  fftd::fft16<1>(u);
+  fftd::fft16<1>(v);
+}
+
+// Two class-r transforms of inputs with stride ld, interleaved (Z dual tasks).
+__device__ __forceinline__ void xform48x2s(const double2* b1, const double2* b2, int ld, int r, double2 (&u)[16],
+                                           double2 (&v)[16]) {
+  u[0] = b1[15 * ld];
+  v[0] = b2[15 * ld];
+  if (r == 0) {
+#pragma unroll
+    for (int m = 1; m < 16; m++) {
+      u[m] = fftd::cadd(b1[(m + 15) * ld], b1[(m - 1) * ld]);
+      v[m] = fftd::cadd(b2[(m + 15) * ld], b2[(m - 1) * ld]);
+    }
+  } else {
+    const double sg = (r == 1) ? -0.86602540378443864676 : 0.86602540378443864676;
+#pragma unroll
+    for (int m = 1; m < 16; m++) {
+      const double2 w = fftd::c_tw48[r * m];
+      const double2 a1 = b1[(m + 15) * ld], c1 = b1[(m - 1) * ld], a2 = b2[(m + 15) * ld], c2 = b2[(m - 1) * ld];
       double2 s1, s2;
       s1.x = fma(-0.5, c1.x, a1.x); s2.x = fma(-0.5, c2.x, a2.x);
       s1.x = fma(-sg, c1.y, s1.x);  s2.x = fma(-sg, c2.y, s2.x);
@@ -1008,6 +1043,7 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
           }
         }
         nbar(3, NZT);  // products complete; tb (and, after the last term, fh) free
+        if (zt == 0 && tg > 0) red_release_add(zcnt + 32 * ((tg - 1) % NB), 1u);  // publish W1(tg - 1)
         if (st) st[2] = clock64();
         if (zt == 0) {
           if (t + 1 < A.T1) issue_tab(t + 1);
@@ -1020,32 +1056,36 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
         nbar(3, NZT);
         if (st) st[3] = clock64();
         double2* W1b = W1t + (tg % NB) * (long long)W1_BUF;
-        // dense task list: tau = r * na + j (na = staged + mirrored pencils); NZT lanes x rounds cover 3 na <= 246
-        const int na = nh + nmir;
+        // dual class tasks: slot s -> class r = s / npair, pencils j1 = s % npair and j2 = j1 + npair (npair =
+        // ceil(na / 2) <= 41, 3 npair <= 123 slots = 2 rounds of 64 threads); two interleaved transforms per thread
+        const int na = nh + nmir, npair = (na + 1) / 2;
 #pragma unroll 1
-        for (int kk = zt; kk < 3 * na + NZT - 1 - ((3 * na + NZT - 1) % NZT); kk += NZT) {
-          const bool act = kk < 3 * na;
-          const int kc = act ? kk : 0;
-          const int r = kc / na, j = kc - r * na;
-          const bool mir = j >= nh;
-          const int jj = mir ? j - nh : j;
-          const double2* Zs = (mir ? zm : zp) + jj;
-          const int pp = mir ? (NPEN - 1) - (h0 + jj) : h0 + jj;
-          double2 u[16];
-          xform48(Zs, nh, r, u);
+        for (int s0 = zt; s0 < 2 * NZT; s0 += NZT) {
+          const bool act = s0 < 3 * npair;
+          const int sc = act ? s0 : 0;
+          const int r = sc / npair, j1 = sc - r * npair, j2 = j1 + npair;
+          const bool act2 = act && j2 < na;
+          const int j2c = act2 ? j2 : j1;
+          const bool mir1 = j1 >= nh, mir2 = j2c >= nh;
+          const int jj1 = mir1 ? j1 - nh : j1, jj2 = mir2 ? j2c - nh : j2c;
+          double2 u[16], v[16];
+          xform48x2s((mir1 ? zm : zp) + jj1, (mir2 ? zm : zp) + jj2, nh, r, u, v);
           if (act) {
+            const int pp1 = mir1 ? (NPEN - 1) - (h0 + jj1) : h0 + jj1;
 #pragma unroll
-            for (int q = 0; q < 16; q++) W1b[(3 * q + r) * NPEN + pp] = u[fftd::qslot(q)];
+            for (int q = 0; q < 16; q++) W1b[(3 * q + r) * NPEN + pp1] = u[fftd::qslot(q)];
+          }
+          if (act2) {
+            const int pp2 = mir2 ? (NPEN - 1) - (h0 + jj2) : h0 + jj2;
+#pragma unroll
+            for (int q = 0; q < 16; q++) W1b[(3 * q + r) * NPEN + pp2] = v[fftd::qslot(q)];
           }
         }
         nbar(3, NZT);
         if (st) st[4] = clock64();
-        if (zt == 0) {
-          __threadfence();
-          atomicAdd(zcnt + 32 * (tg % NB), 1u);  // W1(tg) of this member is published
-        }
       }
     }
+    if (zt == 0 && tg > 0) red_release_add(zcnt + 32 * ((tg - 1) % NB), 1u);  // publish the last term
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
