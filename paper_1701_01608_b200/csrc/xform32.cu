@@ -35,6 +35,18 @@ constexpr int PB2 = 4;  // ky columns per CTA in kb2
 constexpr int RS = 17;  // padded row stride (double2) of 16-element rows
 constexpr int ZS = 49;  // padded row stride (double2) of 48-element rows
 
+// Asynchronous global -> shared copies (LDGSTS): every load of a tile is in flight at once, instead of the few a
+// register-staged loop keeps outstanding (the load phase dominated these HBM/latency-bound kernels).
+__device__ __forceinline__ void cp16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 // smem input adaptors: nz(i) is constant-folded after unrolling
 struct InCol {  // x[i] = base[i * ld], i = 0..n-1, all present
   const double2* base; int ld;
@@ -58,7 +70,8 @@ __global__ void __launch_bounds__(256) kf1(const double* __restrict__ f, double2
   const int jx0 = (blockIdx.x % (N / PL8)) * PL8;
   const double2* src = reinterpret_cast<const double2*>(f + (cell * N + jx0) * N * N);
 #pragma unroll 4
-  for (int i = tid; i < PL8 * N * H; i += 256) buf[(i >> 4) * RS + (i & 15)] = src[i];
+  for (int i = tid; i < PL8 * N * H; i += 256) cp16(buf + (i >> 4) * RS + (i & 15), src + i);
+  cp_wait_all();
   __syncthreads();
   {  // z: thread = (plane, jy)
     double2* row = buf + tid * RS;
@@ -94,8 +107,8 @@ __global__ void __launch_bounds__(256) kf1(const double* __restrict__ f, double2
 // the hot kernel: CTA c of a cell's team of nb CTAs owns pencils [h_c, h_{c+1}), h_c = floor(481 c / nb), stored as
 // [iz][pp - h_c] starting at 31*h_c.  One contiguous block per CTA -> one bulk copy.
 __device__ __forceinline__ int lh_offset(int pp, int iz, int nb) {
-  int c = 0;
-  for (int k = 1; k < nb; k++) c += (pp >= (481 * k) / nb);
+  // member c = max{c : floor(481 c / nb) <= pp} = ceil(nb (pp + 1) / 481) - 1
+  const int c = (nb * (pp + 1) + 480) / 481 - 1;
   const int h0 = (481 * c) / nb, h1 = (481 * (c + 1)) / nb;
   return K * h0 + iz * (h1 - h0) + (pp - h0);
 }
@@ -114,9 +127,10 @@ __global__ void __launch_bounds__(256) kf2(const double2* __restrict__ F2, doubl
     if (g < ncol) {
       const long long cell = g / K;
       const int iy = (int)(g - cell * K);
-      buf[i] = F2[((cell * N + jx) * K + iy) * H + lz];
+      cp16(buf + i, F2 + ((cell * N + jx) * K + iy) * H + lz);
     }
   }
+  cp_wait_all();
   __syncthreads();
   const int r = tid >> 7, p = (tid >> 4) & 7, lz = tid & 15;
   const long long g = g0 + p;
@@ -144,7 +158,7 @@ __global__ void __launch_bounds__(256) kf2(const double2* __restrict__ F2, doubl
 // kb1: CTA = (cell, 4 px planes), 288 threads.  First axis (py, contiguous): two real rows packed as one
 // complex row, FFT48, untangled on the fly (ky = 0..15);  second axis (pz): FFT48 -> kz in K'.
 // Out H2[cell][px][kz][ky].
-__global__ void __launch_bounds__(288) kb1(const double* __restrict__ G, double2* __restrict__ H2) {
+__global__ void __launch_bounds__(288, 2) kb1(const double* __restrict__ G, double2* __restrict__ H2) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   // [4 planes][24 row pairs][ZS]: element py of the pair = (G(pz = 2pr, py), G(pz = 2pr+1, py)); then in
   // place the complex FFT48 of the pair
@@ -158,9 +172,10 @@ __global__ void __launch_bounds__(288) kb1(const double* __restrict__ G, double2
 #pragma unroll 4
     for (int i = tid; i < PB1 * P * P; i += 288) {
       const int row = i / P, col = i - row * P;  // row = s * 48 + pz, col = py
-      dst[((row >> 1) * ZS + col) * 2 + (row & 1)] = src[i];
+      cp8(dst + ((row >> 1) * ZS + col) * 2 + (row & 1), src + i);
     }
   }
+  cp_wait_all();
   __syncthreads();
   {  // z: thread = (class r, plane, row pair)
     const int r = tid / 96, s = (tid % 96) / 24, pr = tid % 24;
@@ -216,9 +231,10 @@ __global__ void __launch_bounds__(192) kb2(const double2* __restrict__ H2, doubl
     if (g < ncol) {
       const long long cell = g / K;
       const int iy = (int)(g - cell * K);
-      buf[i] = H2[((cell * P + px) * K + iy) * H + kz];
+      cp16(buf + i, H2 + ((cell * P + px) * K + iy) * H + kz);
     }
   }
+  cp_wait_all();
   __syncthreads();
   {
     const int r = tid >> 6, p = (tid >> 4) & 3, kz = tid & 15;
@@ -270,9 +286,10 @@ __global__ void __launch_bounds__(256) kb3(const double2* __restrict__ E1, const
 #pragma unroll 4
     for (int i = tid; i < PL8 * K * H; i += 256) {
       const int pl = i / (K * H), rem = i % (K * H);
-      buf[(pl * N + rem / H) * RS + rem % H] = src[i];
+      cp16(buf + (pl * N + rem / H) * RS + rem % H, src + i);
     }
   }
+  cp_wait_all();
   __syncthreads();
   {  // inverse y: thread = (class r, plane, kz)
     const int r = tid >> 7, pl = (tid >> 4) & 7, kz = tid & 15;
@@ -285,9 +302,10 @@ __global__ void __launch_bounds__(256) kb3(const double2* __restrict__ E1, const
     for (int q = 0; q < 16; q++) buf[(pl * N + 2 * q + r) * RS + kz] = u[qslot(q)];
   }
   __syncthreads();
-  {  // z: thread = (plane, jy): X[k] = E2(jy, k), k = 0..15 (X[16] = 0, X[0] taken real)
-    double2* row = buf + tid * RS;
-    double2 x[16], u[16];
+  double2 z[16];
+  {  // y (Hermitian -> real): thread = (plane, jz): X[k] = E2(jz, k), k = 0..15 (X[16] = 0, X[0] taken real)
+    const double2* row = buf + tid * RS;
+    double2 x[16];
 #pragma unroll
     for (int k = 0; k < 16; k++) x[k] = row[k];
     x[0].y = 0.0;
@@ -297,21 +315,34 @@ __global__ void __launch_bounds__(256) kb3(const double2* __restrict__ E1, const
       const double2 b = k == 0 ? make_double2(0.0, 0.0) : make_double2(x[16 - k].x, -x[16 - k].y);  // conj X[16-k]
       const double2 ev = fftd::cadd(a, b);
       const double2 od = k == 0 ? a : fftd::cmul_s<1>(fftd::c_tw32[k], fftd::csub(a, b));
-      u[k] = make_double2(ev.x - od.y, ev.y + od.x);  // ev + i od
+      z[k] = make_double2(ev.x - od.y, ev.y + od.x);  // ev + i od
     }
-    fft16<1>(u);
+    fft16<1>(z);  // z[qslot(n)] = (Q(jy = 2n, jz), Q(jy = 2n + 1, jz))
+  }
+  __syncthreads();  // every row has been read: the region becomes the output staging [plane][jy][OS]
+  constexpr int OS = 33;  // padded jz stride (doubles): conflict-free column writes and row reads
+  double* stg = reinterpret_cast<double*>(smem_raw);
+  {
+    const int pl = tid >> 5, jz = tid & 31;
 #pragma unroll
-    for (int n = 0; n < 16; n++) row[n] = u[qslot(n)];  // (x[2n], x[2n+1])
+    for (int n = 0; n < 16; n++) {
+      stg[(pl * N + 2 * n) * OS + jz] = z[fftd::qslot(n)].x;
+      stg[(pl * N + 2 * n + 1) * OS + jz] = z[fftd::qslot(n)].y;
+    }
   }
   __syncthreads();
-  // buf row (plane, jz) holds (Q(jy = 2n, jz), Q(jy = 2n+1, jz)) at element n: transpose while storing
   const long long base = (cell * N + jx0) * N * N;
-  const double* bd = reinterpret_cast<const double*>(buf);
-#pragma unroll 4
-  for (int i = tid; i < PL8 * N * N; i += 256) {
-    const int pl = i >> 10, jy = (i >> 5) & 31, jz = i & 31;
-    double v = bd[((pl * N + jz) * RS + (jy >> 1)) * 2 + (jy & 1)];
-    if (euler) v = fma(s, v, fin[base + i]);
+  constexpr int PER = PL8 * N * N / 256;  // 32 outputs per thread
+  double fv[PER];
+  if (euler) {  // all loads of f* in flight at once
+#pragma unroll
+    for (int k = 0; k < PER; k++) fv[k] = fin[base + tid + 256 * k];
+  }
+#pragma unroll
+  for (int k = 0; k < PER; k++) {
+    const int i = tid + 256 * k, pl = i >> 10, jy = (i >> 5) & 31, jz = i & 31;
+    double v = stg[(pl * N + jy) * OS + jz];
+    if (euler) v = fma(s, v, fv[k]);
     out[base + i] = v;
   }
 }
@@ -353,6 +384,10 @@ cudaError_t xform32_prepare() {
   if (e == cudaSuccess) e = cudaFuncSetAttribute(kb1, cudaFuncAttributeMaxDynamicSharedMemorySize, PB1 * 24 * ZS * 16);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(kb2, cudaFuncAttributeMaxDynamicSharedMemorySize, PB2 * (P + K) * H * 16);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(kb3, cudaFuncAttributeMaxDynamicSharedMemorySize, PL8 * N * RS * 16);
+  // maximum shared-memory carveout: with the default split kb1 ran one CTA per SM (ncu)
+  const void* ks[] = {(const void*)kf1, (const void*)kf2, (const void*)kb1, (const void*)kb2, (const void*)kb3};
+  for (const void* kk : ks)
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(kk, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
   return e;
 }
 
