@@ -646,10 +646,22 @@ namespace v4 {
 constexpr int TM = 12;                        // CTAs (members) per team = per cell
 constexpr int PLN = P / TM;                   // 4 z-planes per member
 constexpr int NB = 4;                         // W1 team buffers (Z warps run ahead by < NB terms)
+// V4_G4 = 1: 12 warps (2 YX groups of 4 + 4 Z warps, <= 168 registers); 0: 8 warps (2 groups of 3 + 2 Z warps)
+#ifndef V4_G4
+#define V4_G4 1
+#endif
+#if V4_G4
+constexpr int GW = 4;                         // warps per YX group
+#ifndef V4_NZW
+#define V4_NZW 4
+#endif
+#else
+constexpr int GW = 3;
 #ifndef V4_NZW
 #define V4_NZW 2
 #endif
-constexpr int NYX = 6, NZW = V4_NZW;          // YX warps (2 groups of 3), Z warps (3+ Z warps cap registers at 168)
+#endif
+constexpr int NYX = 2 * GW, NZW = V4_NZW;     // YX warps (2 groups of GW), Z warps
 constexpr int NTHR = 32 * (NYX + NZW);        // 288
 constexpr int NZT = 32 * NZW;                 // Z threads
 constexpr int MAXH = 41;                      // max staged pencils per member (481 / 12 rounded up)
@@ -862,7 +874,7 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
 
   if (warp < NYX) {
     // ---------------------------------------------- YX warps ----------------------------------------------
-    const int g = warp / 3, wr = warp - 3 * (warp / 3);
+    const int g = warp / GW, wr = warp - GW * (warp / GW);
     double2* pb0 = reinterpret_cast<double2*>(smem + (2 * g) * PLANE_B);
     double2* pb1 = reinterpret_cast<double2*>(smem + (2 * g + 1) * PLANE_B);
     double2* in0 = pb0;                      // W1 plane 2g
@@ -912,6 +924,59 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
           for (int c = 0; c < 3; c++) tmem_st32(tG + 32 * c, zw);
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         }
+#if V4_G4
+        // 4-warp schedule (15 of 16 slots): R1 Y(c0,p0) Y(c0,p1) Y(c1,p0) Y(c1,p1) | R2 X(0,0) X(0,1) X(0,2) X(1,0)
+        // | R3 X(1,1) X(1,2) Y(c2,p0) Y(c2,p1) | R4 X(2,0) X(2,1) X(2,2) -.  X(c, rx) of warp wr keeps its G block
+        // at TMEM column 32 * blk of the warp's lane quarter (+96 per group).
+#pragma unroll 1
+        for (int rd = 0; rd < 4; rd++) {
+          int kind = 0, c = 0, rx = 0, pl = 0, blk = 0;  // kind 0 idle, 1 Y, 2 X
+          if (rd == 0) { kind = 1; c = wr >> 1; pl = wr & 1; }
+          else if (rd == 1) { kind = 2; c = (wr == 3) ? 1 : 0; rx = (wr == 3) ? 0 : wr; blk = 0; }
+          else if (rd == 2) {
+            if (wr < 2) { kind = 2; c = 1; rx = wr + 1; blk = 1; }
+            else { kind = 1; c = 2; pl = wr - 2; }
+          } else if (wr < 3) { kind = 2; c = 2; rx = wr; blk = (wr == 2) ? 1 : 2; }
+          if (kind != 0) {
+            const double2* base;
+            if (kind == 2) base = ybuf(xp, c == 1 ? 1 : 0) + xq * K;
+            else base = (pl ? in1 : in0) + (lane < K ? lane : K - 1) * K;
+            double2 u[16];
+            xform48(base, 1, kind == 2 ? rx : c, u);
+            if (kind == 2) {
+              g_accumulate(tG + 32u * blk, u);
+              asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            } else if (lane < K) {
+              double2* ydst = ybuf(pl, c == 1 ? 1 : 0) + lane;
+#pragma unroll
+              for (int q = 0; q < 16; q++) ydst[q * K] = u[fftd::qslot(q)];
+            }
+          }
+          nbar(1 + g, 32 * GW);
+          if (st) st[2 + rd] = clock64();
+          if (rd == 2 && leader && tg + 1 < total_tg &&
+              ld_acquire(zcnt + 32 * ((tg + 1) % NB)) >= (unsigned)(TM * ((tg + 1) / NB + 1))) {
+            issue_w1(tg + 1);  // input planes are free: overlap the copy with R4
+            issued = true;
+          }
+        }
+        if (t == A.T1 - 1) {  // G[cell][px = 3q' + rx][pz][py = 3 xq + c] for each block of this warp
+          double* Gc = A.G + cell * (long long)(P * P * P) + (long long)(pz0 + xp) * P;
+          const int nblk = (wr < 2) ? 3 : (wr == 2 ? 2 : 1);
+#pragma unroll 1
+          for (int bl = 0; bl < nblk; bl++) {
+            int c, rx;
+            if (wr < 2) { c = bl; rx = (bl == 1) ? wr + 1 : wr; }
+            else if (wr == 2) { c = (bl == 0) ? 0 : 2; rx = 2; }
+            else { c = 1; rx = 0; }
+            uint32_t gw[32];
+            tmem_ld32(tG + 32 * bl, gw);
+#pragma unroll
+            for (int q = 0; q < 16; q++)
+              Gc[(long long)(3 * q + rx) * P * P + 3 * xq + c] = __hiloint2double((int)gw[2 * q + 1], (int)gw[2 * q]);
+          }
+        }
+#else
 #pragma unroll 1
         for (int rd = 0; rd < 4; rd++) {
           // task of this warp in round rd (see the schedule above; rd == 3 fuses R4 and R5)
@@ -921,7 +986,7 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
             g_accumulate(tG + 32u, u);
             g_accumulate(tG + 64u, v);
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-            nbar(1 + g, 96);
+            nbar(1 + g, 32 * GW);
             if (st) st[5] = clock64();
             break;
           }
@@ -970,6 +1035,7 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
               Gc[(long long)(3 * q + wr) * P * P + 3 * xq + c] = __hiloint2double((int)gw[2 * q + 1], (int)gw[2 * q]);
           }
         }
+#endif
       }
     }
   } else {
@@ -1056,6 +1122,26 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
         nbar(3, NZT);
         if (st) st[3] = clock64();
         double2* W1b = W1t + (tg % NB) * (long long)W1_BUF;
+#if V4_G4
+        {  // 4 Z warps: single class tasks tau = r * na + j, 2 rounds of 128 threads cover 3 na <= 246
+          const int na = nh + nmir;
+#pragma unroll 1
+          for (int kk = zt; kk < 2 * NZT; kk += NZT) {
+            const bool act = kk < 3 * na;
+            const int kc = act ? kk : 0;
+            const int r = kc / na, j = kc - r * na;
+            const bool mir = j >= nh;
+            const int jj = mir ? j - nh : j;
+            double2 u[16];
+            xform48((mir ? zm : zp) + jj, nh, r, u);
+            if (act) {
+              const int pp = mir ? (NPEN - 1) - (h0 + jj) : h0 + jj;
+#pragma unroll
+              for (int q = 0; q < 16; q++) W1b[(3 * q + r) * NPEN + pp] = u[fftd::qslot(q)];
+            }
+          }
+        }
+#else
         // dual class tasks: slot s -> class r = s / npair, pencils j1 = s % npair and j2 = j1 + npair (npair =
         // ceil(na / 2) <= 41, 3 npair <= 123 slots = 2 rounds of 64 threads); two interleaved transforms per thread
         const int na = nh + nmir, npair = (na + 1) / 2;
@@ -1081,6 +1167,7 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
             for (int q = 0; q < 16; q++) W1b[(3 * q + r) * NPEN + pp2] = v[fftd::qslot(q)];
           }
         }
+#endif
         nbar(3, NZT);
         if (st) st[4] = clock64();
       }
