@@ -669,10 +669,15 @@ constexpr int ZSLOT = 96;                     // Z task slots per output class (
 constexpr int YB = 16 * K;                    // complex elements of one Y class buffer [16 rows][31]
 constexpr int W1IN_B = NPEN * 16;             // 15376 B: one W1 plane
 constexpr int YBUF_B = YB * 16;               // 7936 B
-constexpr int PLANE_B = W1IN_B + 2 * YBUF_B;  // 31248 B per owned plane
+#if V4_G4
+constexpr int NYSLOT = 3;                     // Y class slots per plane (one per class: Y(c) never waits for X(c'))
+#else
+constexpr int NYSLOT = 2;                     // slot 0: class 0 then 2, slot 1: class 1
+#endif
+constexpr int PLANE_B = W1IN_B + NYSLOT * YBUF_B;  // per owned plane
 constexpr int ZBLK_B = K * MAXH * 16;         // 20336 B
 constexpr int OFF_Z = PLN * PLANE_B;          // 124992
-constexpr int SMEM_B = OFF_Z + 4 * ZBLK_B;    // 206336 B
+constexpr int SMEM_B = OFF_Z + 2 * ZBLK_B;    // Z product buffers only (f^ and tables are read from L2)
 constexpr int CTR_STRIDE = 256;               // counter words per team (one 128-B line per counter)
 // Synchronisation (exact because buffer b = tg % NB is refilled only after all consumers of its previous
 // generation acknowledged it):  W1(tg) is complete when zcnt[b] == TM (tg / NB + 1);  buffer b may be
@@ -707,6 +712,7 @@ __device__ __forceinline__ void poll_ge(const unsigned* p, unsigned target) {
 __device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
   asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ int vload(const int* p) { return *reinterpret_cast<const volatile int*>(p); }
 __device__ __forceinline__ void nbar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
 __device__ __forceinline__ void tmem_ld32(uint32_t addr, uint32_t (&v)[32]) {
@@ -844,6 +850,8 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
   __shared__ uint32_t tmem_base_sh;
   __shared__ __align__(8) uint64_t bar_w1[2];
   __shared__ __align__(8) uint64_t bar_tab, bar_fh;
+  // YX groups (V4_G4): per-group completion counters instead of round barriers
+  __shared__ int s_yc[2][3], s_xc[2][3], s_yall[2], s_w1iss[2];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int team = blockIdx.x / TM, k = blockIdx.x - (blockIdx.x / TM) * TM;
   constexpr int NLOW = NPEN / 2 + 1;
@@ -866,6 +874,9 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
     mbar_init(&bar_w1[1]);
     mbar_init(&bar_tab);
     mbar_init(&bar_fh);
+    for (int i = 0; i < 6; i++) { (&s_yc[0][0])[i] = 0; (&s_xc[0][0])[i] = 0; }
+    s_yall[0] = s_yall[1] = 0;
+    s_w1iss[0] = s_w1iss[1] = 0;
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -904,6 +915,120 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
         long long* st = (A.dbg && leader && g == 0 && cell == team && t >= 2 && t < 6)
                             ? A.dbg + (long long)blockIdx.x * 128 + (t - 2) * 16 : nullptr;
         if (st) st[0] = clock64();
+#if V4_G4
+        // Static per-warp task lists, synchronised by per-group completion counters (no round barriers):
+        //   wr0: Y(0,p0) Y(2,p0) X(0,0) X(1,1)    wr1: Y(0,p1) Y(2,p1) X(0,1) X(2,0)
+        //   wr2: Y(1,p0) X(0,2) X(2,1)            wr3: Y(1,p1) X(1,0) X(1,2) X(2,2)
+        // One Y slot per class: Y(t, c, p) waits only for X(t-1, c, *) to have read slot c, X(t, c, rx) for both
+        // planes of class c, so terms overlap.  X(c,rx) of a warp keeps its G block at TMEM column 32 * blk of the
+        // warp's lane quarter (+96 per group).
+        int* yc = s_yc[g];
+        int* xc = s_xc[g];
+        auto wait_ge = [&](const int* ptr, int target) {
+          if (lane == 0) {
+            long long spins = 0;
+            while (vload(ptr) < target) {
+              __nanosleep(32);
+              if (++spins > (1LL << 26)) asm volatile("trap;");
+            }
+          }
+          __syncwarp();
+        };
+        auto try_issue_w1 = [&](long long tz, bool block) {  // lane 0 only: bulk-copy W1(tz) (once per group)
+          if (tz >= total_tg) return;
+          if (vload(&s_w1iss[g]) > (int)tz) return;
+          if (vload(&s_yall[g]) < 6 * (int)tz) {  // input planes still read by Y(tz - 1)
+            if (!block) return;
+            long long spins = 0;
+            while (vload(&s_yall[g]) < 6 * (int)tz) { __nanosleep(32); if (++spins > (1LL << 26)) asm volatile("trap;"); }
+          }
+          unsigned* zc = zcnt + 32 * (tz % NB);
+          const unsigned target = (unsigned)(TM * (tz / NB + 1));
+          if (block) poll_ge(zc, target);
+          else if (ld_acquire(zc) < target) return;
+          if (atomicCAS(&s_w1iss[g], (int)tz, (int)tz + 1) == (int)tz) issue_w1(tz);
+        };
+        if (lane == 0 && wr == 0) try_issue_w1(tg, true);
+        if (st) st[1] = clock64();
+        bool w1_seen = false;
+#pragma unroll 1
+        for (int ti = 0; ti < 4; ti++) {
+          int kind = 0, c = 0, rx = 0, pl = 0, blk = 0;  // kind 1 Y, 2 X
+          if (wr == 0) {         // Y(0,p0) Y(2,p0) X(0,0) X(1,1)
+            if (ti < 2) { kind = 1; c = 2 * ti; pl = 0; }
+            else { kind = 2; c = ti - 2; rx = ti - 2; blk = ti - 2; }
+          } else if (wr == 1) {  // Y(0,p1) Y(2,p1) X(0,1) X(2,0)
+            if (ti < 2) { kind = 1; c = 2 * ti; pl = 1; }
+            else if (ti == 2) { kind = 2; c = 0; rx = 1; blk = 0; }
+            else { kind = 2; c = 2; rx = 0; blk = 1; }
+          } else if (wr == 2) {  // Y(1,p0) X(0,2) X(2,1)
+            if (ti == 0) { kind = 1; c = 1; pl = 0; }
+            else if (ti == 1) { kind = 2; c = 0; rx = 2; blk = 0; }
+            else if (ti == 2) { kind = 2; c = 2; rx = 1; blk = 1; }
+          } else {               // Y(1,p1) X(1,0) X(1,2) X(2,2)
+            if (ti == 0) { kind = 1; c = 1; pl = 1; }
+            else { kind = 2; c = ti == 3 ? 2 : 1; rx = ti == 1 ? 0 : 2; blk = ti - 1; }
+          }
+          if (kind == 0) continue;
+          const int T = (int)tg;
+          if (kind == 1) {
+            if (!w1_seen) {
+              mbar_wait(&bar_w1[g], par);
+              w1_seen = true;
+              if (leader) {
+                __threadfence();
+                atomicAdd(ycnt + 32 * (tg % NB), 1u);  // this group has consumed W1(tg)
+              }
+            }
+            wait_ge(&xc[c], 3 * T);  // slot c last read by X(t-1, c, *)
+          } else {
+            wait_ge(&yc[c], 2 * (T + 1));
+            if (t == 0) {  // first term of the cell: zero this block
+              uint32_t zw[32];
+#pragma unroll
+              for (int i = 0; i < 32; i++) zw[i] = 0u;
+              tmem_st32(tG + 32u * blk, zw);
+              asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            }
+          }
+          const double2* base;
+          if (kind == 2) base = ybuf(xp, c) + xq * K;
+          else base = (pl ? in1 : in0) + (lane < K ? lane : K - 1) * K;
+          double2 u[16];
+          xform48(base, 1, kind == 2 ? rx : c, u);
+          if (kind == 2) {
+            g_accumulate(tG + 32u * blk, u);
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            if (t == A.T1 - 1) {  // last term of the cell: G[cell][px = 3q' + rx][pz][py = 3 xq + c]
+              double* Gc = A.G + cell * (long long)(P * P * P) + (long long)(pz0 + xp) * P;
+              uint32_t gw[32];
+              tmem_ld32(tG + 32u * blk, gw);
+#pragma unroll
+              for (int q = 0; q < 16; q++)
+                Gc[(long long)(3 * q + rx) * P * P + 3 * xq + c] = __hiloint2double((int)gw[2 * q + 1], (int)gw[2 * q]);
+            }
+            __syncwarp();
+            if (lane == 0) {
+              __threadfence_block();
+              atomicAdd(&xc[c], 1);
+            }
+          } else {
+            if (lane < K) {
+              double2* ydst = ybuf(pl, c) + lane;
+#pragma unroll
+              for (int q = 0; q < 16; q++) ydst[q * K] = u[fftd::qslot(q)];
+            }
+            __syncwarp();
+            if (lane == 0) {
+              __threadfence_block();
+              atomicAdd(&yc[c], 1);
+              if (atomicAdd(&s_yall[g], 1) + 1 == 6 * (T + 1)) try_issue_w1(tg + 1, false);  // prefetch
+            }
+          }
+        }
+        par ^= 1;
+        if (st) st[5] = clock64();
+#else
         if (leader && !issued) {
           poll_ge(zcnt + 32 * (tg % NB), (unsigned)(TM * (tg / NB + 1)));
           issue_w1(tg);
@@ -924,59 +1049,6 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
           for (int c = 0; c < 3; c++) tmem_st32(tG + 32 * c, zw);
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         }
-#if V4_G4
-        // 4-warp schedule (15 of 16 slots): R1 Y(c0,p0) Y(c0,p1) Y(c1,p0) Y(c1,p1) | R2 X(0,0) X(0,1) X(0,2) X(1,0)
-        // | R3 X(1,1) X(1,2) Y(c2,p0) Y(c2,p1) | R4 X(2,0) X(2,1) X(2,2) -.  X(c, rx) of warp wr keeps its G block
-        // at TMEM column 32 * blk of the warp's lane quarter (+96 per group).
-#pragma unroll 1
-        for (int rd = 0; rd < 4; rd++) {
-          int kind = 0, c = 0, rx = 0, pl = 0, blk = 0;  // kind 0 idle, 1 Y, 2 X
-          if (rd == 0) { kind = 1; c = wr >> 1; pl = wr & 1; }
-          else if (rd == 1) { kind = 2; c = (wr == 3) ? 1 : 0; rx = (wr == 3) ? 0 : wr; blk = 0; }
-          else if (rd == 2) {
-            if (wr < 2) { kind = 2; c = 1; rx = wr + 1; blk = 1; }
-            else { kind = 1; c = 2; pl = wr - 2; }
-          } else if (wr < 3) { kind = 2; c = 2; rx = wr; blk = (wr == 2) ? 1 : 2; }
-          if (kind != 0) {
-            const double2* base;
-            if (kind == 2) base = ybuf(xp, c == 1 ? 1 : 0) + xq * K;
-            else base = (pl ? in1 : in0) + (lane < K ? lane : K - 1) * K;
-            double2 u[16];
-            xform48(base, 1, kind == 2 ? rx : c, u);
-            if (kind == 2) {
-              g_accumulate(tG + 32u * blk, u);
-              asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-            } else if (lane < K) {
-              double2* ydst = ybuf(pl, c == 1 ? 1 : 0) + lane;
-#pragma unroll
-              for (int q = 0; q < 16; q++) ydst[q * K] = u[fftd::qslot(q)];
-            }
-          }
-          nbar(1 + g, 32 * GW);
-          if (st) st[2 + rd] = clock64();
-          if (rd == 2 && leader && tg + 1 < total_tg &&
-              ld_acquire(zcnt + 32 * ((tg + 1) % NB)) >= (unsigned)(TM * ((tg + 1) / NB + 1))) {
-            issue_w1(tg + 1);  // input planes are free: overlap the copy with R4
-            issued = true;
-          }
-        }
-        if (t == A.T1 - 1) {  // G[cell][px = 3q' + rx][pz][py = 3 xq + c] for each block of this warp
-          double* Gc = A.G + cell * (long long)(P * P * P) + (long long)(pz0 + xp) * P;
-          const int nblk = (wr < 2) ? 3 : (wr == 2 ? 2 : 1);
-#pragma unroll 1
-          for (int bl = 0; bl < nblk; bl++) {
-            int c, rx;
-            if (wr < 2) { c = bl; rx = (bl == 1) ? wr + 1 : wr; }
-            else if (wr == 2) { c = (bl == 0) ? 0 : 2; rx = 2; }
-            else { c = 1; rx = 0; }
-            uint32_t gw[32];
-            tmem_ld32(tG + 32 * bl, gw);
-#pragma unroll
-            for (int q = 0; q < 16; q++)
-              Gc[(long long)(3 * q + rx) * P * P + 3 * xq + c] = __hiloint2double((int)gw[2 * q + 1], (int)gw[2 * q]);
-          }
-        }
-#else
 #pragma unroll 1
         for (int rd = 0; rd < 4; rd++) {
           // task of this warp in round rd (see the schedule above; rd == 3 fuses R4 and R5)
@@ -1041,70 +1113,49 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
   } else {
     // ---------------------------------------------- Z warps -----------------------------------------------
     const int zt = tid - 32 * NYX;  // 0..NZT-1
-    double2* fh = reinterpret_cast<double2*>(smem + OFF_Z);
-    double2* tb = reinterpret_cast<double2*>(smem + OFF_Z + ZBLK_B);
-    double2* zp = reinterpret_cast<double2*>(smem + OFF_Z + 2 * ZBLK_B);
-    double2* zm = reinterpret_cast<double2*>(smem + OFF_Z + 3 * ZBLK_B);
-    const uint32_t blk = (uint32_t)(K * nh) * 16u;
-    auto issue_tab = [&](int t) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_expect(&bar_tab, blk);
-      bulk_g2s(tb, A.tabT + (long long)t * LHN + K * h0, blk, &bar_tab);
-    };
-    auto issue_fh = [&](long long cell) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_expect(&bar_fh, blk);
-      bulk_g2s(fh, A.fhatT + cell * (long long)LHN + K * h0, blk, &bar_fh);
-    };
-    if (zt == 0 && ncell_team > 0) {
-      issue_fh(team);
-      issue_tab(0);
-    }
-    uint32_t par_tab = 0, par_fh = 0;
+    double2* zp = reinterpret_cast<double2*>(smem + OFF_Z);
+    double2* zm = reinterpret_cast<double2*>(smem + OFF_Z + ZBLK_B);
     long long tg = 0;
 #pragma unroll 1
     for (long long cell = team; cell < A.n_cells; cell += A.nteams) {
-      mbar_wait(&bar_fh, par_fh);
-      par_fh ^= 1;
+      const double2* fh = A.fhatT + cell * (long long)LHN + K * h0;  // the member's f^ block (L2)
 #pragma unroll 1
       for (int t = 0; t < A.T1; t++, tg++) {
+        const double2* tb = A.tabT + (long long)t * LHN + K * h0;     // the member's table block (L2)
         long long* st = (A.dbg && zt == 0 && cell == team && t >= 2 && t < 6)
                             ? A.dbg + (long long)blockIdx.x * 128 + (t - 2) * 16 + 8 : nullptr;
         if (st) st[0] = clock64();
-        mbar_wait(&bar_tab, par_tab);
-        par_tab ^= 1;
         if (st) st[1] = clock64();
         // products: Z = (a + ib) f^ for the staged pencils, and for their mirrors (-lx,-ly): (a + ib) conj(f^)
         // at the reversed lz (a, b even; f real)
         {  // element pairs {i, 30 - i} of pencil j, e = i * nh + j; i = e / nh by multiply-high (exact: e nh < 2^32).
            // Four iterations are loaded before any store (the product buffers never alias the staged inputs).
           const unsigned mdiv = 0xffffffffu / (unsigned)nh + 1u;
-          const double2* __restrict__ fr = fh;
+          const double2* __restrict__ fr = fh;  // read-only global (L2-resident)
           const double2* __restrict__ tr = tb;
           double2* __restrict__ pw = zp;
           double2* __restrict__ mw = zm;
           const int ne = 16 * nh;
-#pragma unroll 1
-          for (int e0 = zt; e0 < ne; e0 += 4 * NZT) {
-            double2 f1[4], a1[4], f2[4], a2[4];
-            int o1[4], o2[4];
+          // every load of this thread (<= ZIT iterations) is issued before the first product: one L2 round trip
+          constexpr int ZIT = (16 * MAXH + NZT - 1) / NZT;
+          double2 f1[ZIT], a1[ZIT], f2[ZIT], a2[ZIT];
+          int o1[ZIT], o2[ZIT];
 #pragma unroll
-            for (int u = 0; u < 4; u++) {
-              const int e = min(e0 + u * NZT, ne - 1);
-              const int i = (int)__umulhi((unsigned)e, mdiv), j = e - i * nh;
-              o1[u] = i * nh + j;
-              o2[u] = (30 - i) * nh + j;
-              f1[u] = fr[o1[u]]; a1[u] = tr[o1[u]];
-              f2[u] = fr[o2[u]]; a2[u] = tr[o2[u]];
-            }
+          for (int u = 0; u < ZIT; u++) {
+            const int e = min(zt + u * NZT, ne - 1);
+            const int i = (int)__umulhi((unsigned)e, mdiv), j = e - i * nh;
+            o1[u] = i * nh + j;
+            o2[u] = (30 - i) * nh + j;
+            f1[u] = __ldg(fr + o1[u]); a1[u] = __ldg(tr + o1[u]);
+            f2[u] = __ldg(fr + o2[u]); a2[u] = __ldg(tr + o2[u]);
+          }
 #pragma unroll
-            for (int u = 0; u < 4; u++) {
-              if (e0 + u * NZT < ne) {
-                pw[o1[u]] = make_double2(fma(a1[u].x, f1[u].x, -a1[u].y * f1[u].y), fma(a1[u].x, f1[u].y, a1[u].y * f1[u].x));
-                pw[o2[u]] = make_double2(fma(a2[u].x, f2[u].x, -a2[u].y * f2[u].y), fma(a2[u].x, f2[u].y, a2[u].y * f2[u].x));
-                mw[o1[u]] = make_double2(fma(a2[u].x, f2[u].x, a2[u].y * f2[u].y), fma(-a2[u].x, f2[u].y, a2[u].y * f2[u].x));
-                mw[o2[u]] = make_double2(fma(a1[u].x, f1[u].x, a1[u].y * f1[u].y), fma(-a1[u].x, f1[u].y, a1[u].y * f1[u].x));
-              }
+          for (int u = 0; u < ZIT; u++) {
+            if (zt + u * NZT < ne) {
+              pw[o1[u]] = make_double2(fma(a1[u].x, f1[u].x, -a1[u].y * f1[u].y), fma(a1[u].x, f1[u].y, a1[u].y * f1[u].x));
+              pw[o2[u]] = make_double2(fma(a2[u].x, f2[u].x, -a2[u].y * f2[u].y), fma(a2[u].x, f2[u].y, a2[u].y * f2[u].x));
+              mw[o1[u]] = make_double2(fma(a2[u].x, f2[u].x, a2[u].y * f2[u].y), fma(-a2[u].x, f2[u].y, a2[u].y * f2[u].x));
+              mw[o2[u]] = make_double2(fma(a1[u].x, f1[u].x, a1[u].y * f1[u].y), fma(-a1[u].x, f1[u].y, a1[u].y * f1[u].x));
             }
           }
         }
@@ -1112,11 +1163,6 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
         if (zt == 0 && tg > 0) red_release_add(zcnt + 32 * ((tg - 1) % NB), 1u);  // publish W1(tg - 1)
         if (st) st[2] = clock64();
         if (zt == 0) {
-          if (t + 1 < A.T1) issue_tab(t + 1);
-          else if (cell + A.nteams < A.n_cells) {
-            issue_fh(cell + A.nteams);
-            issue_tab(0);
-          }
           if (tg >= NB) poll_ge(ycnt + 32 * (tg % NB), (unsigned)(2 * TM * (tg / NB)));  // buffer free
         }
         nbar(3, NZT);
