@@ -646,11 +646,24 @@ namespace v4 {
 constexpr int TM = 12;                        // CTAs (members) per team = per cell
 constexpr int PLN = P / TM;                   // 4 z-planes per member
 constexpr int NB = 4;                         // W1 team buffers (Z warps run ahead by < NB terms)
-// V4_G4 = 1: 12 warps (2 YX groups of 4 + 4 Z warps, <= 168 registers); 0: 8 warps (2 groups of 3 + 2 Z warps)
+// V4_G6 = 1: 16 warps (2 YX groups of 6 + 4 Z warps, <= 128 registers)
+// V4_G4 = 1: 12 warps (2 YX groups of 4 + 4 Z warps, <= 168 registers); both 0: 8 warps (groups of 3 + 2 Z warps)
+#ifndef V4_G6
+#define V4_G6 1
+#endif
+#if V4_G6
+#undef V4_G4
+#define V4_G4 1
+#endif
 #ifndef V4_G4
 #define V4_G4 1
 #endif
-#if V4_G4
+#if V4_G6
+constexpr int GW = 6;                         // warps per YX group
+#ifndef V4_NZW
+#define V4_NZW 4
+#endif
+#elif V4_G4
 constexpr int GW = 4;                         // warps per YX group
 #ifndef V4_NZW
 #define V4_NZW 4
@@ -677,7 +690,7 @@ constexpr int NYSLOT = 2;                     // slot 0: class 0 then 2, slot 1:
 constexpr int PLANE_B = W1IN_B + NYSLOT * YBUF_B;  // per owned plane
 constexpr int ZBLK_B = K * MAXH * 16;         // 20336 B
 constexpr int OFF_Z = PLN * PLANE_B;          // 124992
-constexpr int SMEM_B = OFF_Z + 2 * ZBLK_B;    // Z product buffers only (f^ and tables are read from L2)
+constexpr int SMEM_B = OFF_Z + 3 * ZBLK_B;    // Z: products (2) + the cell's f^ block (tables are read from L2)
 constexpr int CTR_STRIDE = 256;               // counter words per team (one 128-B line per counter)
 // Synchronisation (exact because buffer b = tg % NB is refilled only after all consumers of its previous
 // generation acknowledged it):  W1(tg) is complete when zcnt[b] == TM (tg / NB + 1);  buffer b may be
@@ -893,7 +906,11 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
     // Y class slots: slot 0 holds row class 0 then 2, slot 1 row class 1; plane 2g at pb0, 2g+1 at pb1
     auto ybuf = [&](int pl, int slot) { return (pl ? pb1 : pb0) + NPEN + slot * YB; };
     const int pz0 = PLN * k + 2 * g;
+#if V4_G6
+    const uint32_t tG = tbase + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(64 * (warp >> 2));  // <= 2 blocks
+#else
     const uint32_t tG = tbase + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(96 * g);
+#endif
     const bool leader = (wr == 0 && lane == 0);
     auto issue_w1 = [&](long long tgi) {
       const double2* src = W1t + (tgi % NB) * (long long)W1_BUF + (long long)pz0 * NPEN;
@@ -951,9 +968,27 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
         if (lane == 0 && wr == 0) try_issue_w1(tg, true);
         if (st) st[1] = clock64();
         bool w1_seen = false;
+#if V4_G6
+        constexpr int NTASK = 3;
+#else
+        constexpr int NTASK = 4;
+#endif
 #pragma unroll 1
-        for (int ti = 0; ti < 4; ti++) {
+        for (int ti = 0; ti < NTASK; ti++) {
           int kind = 0, c = 0, rx = 0, pl = 0, blk = 0;  // kind 1 Y, 2 X
+#if V4_G6
+          // wr0: Y(0,p0) X(0,0) X(2,1)   wr1: Y(0,p1) X(0,1) X(2,2)   wr2: Y(1,p0) X(0,2)
+          // wr3: Y(1,p1) X(1,0)          wr4: Y(2,p0) X(1,1)          wr5: Y(2,p1) X(1,2) X(2,0)
+          if (ti == 0) { kind = 1; c = wr >> 1; pl = wr & 1; }
+          else if (ti == 1) {
+            kind = 2; blk = 0;
+            c = wr < 3 ? 0 : 1;
+            rx = wr < 3 ? wr : wr - 3;
+          } else if (wr == 0 || wr == 1 || wr == 5) {
+            kind = 2; blk = 1; c = 2;
+            rx = wr == 0 ? 1 : (wr == 1 ? 2 : 0);
+          }
+#else
           if (wr == 0) {         // Y(0,p0) Y(2,p0) X(0,0) X(1,1)
             if (ti < 2) { kind = 1; c = 2 * ti; pl = 0; }
             else { kind = 2; c = ti - 2; rx = ti - 2; blk = ti - 2; }
@@ -969,6 +1004,7 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
             if (ti == 0) { kind = 1; c = 1; pl = 1; }
             else { kind = 2; c = ti == 3 ? 2 : 1; rx = ti == 1 ? 0 : 2; blk = ti - 1; }
           }
+#endif
           if (kind == 0) continue;
           const int T = (int)tg;
           if (kind == 1) {
@@ -1115,10 +1151,20 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
     const int zt = tid - 32 * NYX;  // 0..NZT-1
     double2* zp = reinterpret_cast<double2*>(smem + OFF_Z);
     double2* zm = reinterpret_cast<double2*>(smem + OFF_Z + ZBLK_B);
+    double2* fh = reinterpret_cast<double2*>(smem + OFF_Z + 2 * ZBLK_B);  // the cell's f^ block (TMA, per cell)
+    const uint32_t fblk = (uint32_t)(K * nh) * 16u;
+    auto issue_fh = [&](long long cl) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_expect(&bar_fh, fblk);
+      bulk_g2s(fh, A.fhatT + cl * (long long)LHN + K * h0, fblk, &bar_fh);
+    };
+    if (zt == 0 && ncell_team > 0) issue_fh(team);
+    uint32_t par_fh = 0;
     long long tg = 0;
 #pragma unroll 1
     for (long long cell = team; cell < A.n_cells; cell += A.nteams) {
-      const double2* fh = A.fhatT + cell * (long long)LHN + K * h0;  // the member's f^ block (L2)
+      mbar_wait(&bar_fh, par_fh);
+      par_fh ^= 1;
 #pragma unroll 1
       for (int t = 0; t < A.T1; t++, tg++) {
         const double2* tb = A.tabT + (long long)t * LHN + K * h0;     // the member's table block (L2)
@@ -1131,35 +1177,42 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
         {  // element pairs {i, 30 - i} of pencil j, e = i * nh + j; i = e / nh by multiply-high (exact: e nh < 2^32).
            // Four iterations are loaded before any store (the product buffers never alias the staged inputs).
           const unsigned mdiv = 0xffffffffu / (unsigned)nh + 1u;
-          const double2* __restrict__ fr = fh;  // read-only global (L2-resident)
+          const double2* __restrict__ fr = fh;  // f^ block in shared memory
           const double2* __restrict__ tr = tb;
           double2* __restrict__ pw = zp;
           double2* __restrict__ mw = zm;
           const int ne = 16 * nh;
           // every load of this thread (<= ZIT iterations) is issued before the first product: one L2 round trip
-          constexpr int ZIT = (16 * MAXH + NZT - 1) / NZT;
+          constexpr int ZIT = (16 * MAXH + NZT - 1) / NZT;  // all table loads of this thread in one L2 round
+#pragma unroll 1
+          for (int zb = 0; zb * ZIT * NZT < ne; zb++) {
+          const int zt0 = zt + zb * ZIT * NZT;
           double2 f1[ZIT], a1[ZIT], f2[ZIT], a2[ZIT];
           int o1[ZIT], o2[ZIT];
 #pragma unroll
           for (int u = 0; u < ZIT; u++) {
-            const int e = min(zt + u * NZT, ne - 1);
+            const int e = min(zt0 + u * NZT, ne - 1);
             const int i = (int)__umulhi((unsigned)e, mdiv), j = e - i * nh;
             o1[u] = i * nh + j;
             o2[u] = (30 - i) * nh + j;
-            f1[u] = __ldg(fr + o1[u]); a1[u] = __ldg(tr + o1[u]);
-            f2[u] = __ldg(fr + o2[u]); a2[u] = __ldg(tr + o2[u]);
+            a1[u] = __ldg(tr + o1[u]);
+            a2[u] = __ldg(tr + o2[u]);
           }
 #pragma unroll
           for (int u = 0; u < ZIT; u++) {
-            if (zt + u * NZT < ne) {
+            f1[u] = fr[o1[u]];  // shared memory
+            f2[u] = fr[o2[u]];
+            if (zt0 + u * NZT < ne) {
               pw[o1[u]] = make_double2(fma(a1[u].x, f1[u].x, -a1[u].y * f1[u].y), fma(a1[u].x, f1[u].y, a1[u].y * f1[u].x));
               pw[o2[u]] = make_double2(fma(a2[u].x, f2[u].x, -a2[u].y * f2[u].y), fma(a2[u].x, f2[u].y, a2[u].y * f2[u].x));
               mw[o1[u]] = make_double2(fma(a2[u].x, f2[u].x, a2[u].y * f2[u].y), fma(-a2[u].x, f2[u].y, a2[u].y * f2[u].x));
               mw[o2[u]] = make_double2(fma(a1[u].x, f1[u].x, a1[u].y * f1[u].y), fma(-a1[u].x, f1[u].y, a1[u].y * f1[u].x));
             }
           }
+          }
         }
-        nbar(3, NZT);  // products complete; tb (and, after the last term, fh) free
+        nbar(3, NZT);  // products complete (after the cell's last term the f^ block is free)
+        if (zt == 0 && t == A.T1 - 1 && cell + A.nteams < A.n_cells) issue_fh(cell + A.nteams);
         if (zt == 0 && tg > 0) red_release_add(zcnt + 32 * ((tg - 1) % NB), 1u);  // publish W1(tg - 1)
         if (st) st[2] = clock64();
         if (zt == 0) {
