@@ -62,6 +62,7 @@ struct Ctx {
   double* d_stage_out = nullptr;
   long long stage_cells = 0;
   cudaStream_t stage_stream = nullptr;
+  cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;  // host-buffer step pipeline
   // transport state (generic cell)
   bool transport_ready = false;
   int nx = 0, ny = 0, nz = 0;
@@ -102,6 +103,7 @@ size_t fast_ws_bytes_per_cell(const Ctx& c);
 fks_status fast_prepare(Ctx& c);
 
 // transport gather (transport.cu)
-fks_status launch_transport_gather(Ctx& c, const double* fin, double* fout, const Shift& sh, cudaStream_t st);
+fks_status launch_transport_gather(Ctx& c, const double* fin, double* fout, const Shift& sh, cudaStream_t st,
+                                   long long cell0 = 0, long long ncells = -1);
 
 }  // namespace fks

@@ -355,21 +355,72 @@ fks_status fks_collision_batch_host(fks_ctx* h, const double* f_host, double* Q_
   return cuda_status(cudaStreamSynchronize(st), "host-buffer collision");
 }
 
+// Host-buffer step, pipelined over slabs of x-planes on three streams: the input planes are copied in (the
+// periodic wrap-around halo first), each slab is transported and collided as soon as the planes it gathers from
+// (slab +- max |delta_x|) have landed, and each finished slab is copied back while the next one computes.
 fks_status fks_step_host(fks_ctx* h, const double* f_in_host, double* f_out_host, double coll_scale) {
   if (!h) { set_error("NULL handle"); return FKS_ERR_INVALID; }
   Ctx& c = *reinterpret_cast<Ctx*>(h);
   if (!c.transport_ready) { set_error("fks_transport_setup not called"); return FKS_ERR_STATE; }
   if (!f_in_host || !f_out_host) { set_error("bad host buffers"); return FKS_ERR_INVALID; }
-  long long n = (long long)c.nx * c.ny * c.nz;
+  if (!std::isfinite(coll_scale)) { set_error("coll_scale must be finite"); return FKS_ERR_INVALID; }
+  const long long n = (long long)c.nx * c.ny * c.nz;
   fks_status rc;
   if ((rc = sticky_check())) return rc;
   if ((rc = ensure_stage(c, n))) return rc;
-  const size_t bytes = (size_t)n * c.N * c.N * c.N * sizeof(double);
+  if (!c.h2d_stream) cudaStreamCreateWithFlags(&c.h2d_stream, cudaStreamNonBlocking);
+  if (!c.d2h_stream) cudaStreamCreateWithFlags(&c.d2h_stream, cudaStreamNonBlocking);
+  const long long nv = (long long)c.N * c.N * c.N;
+  const long long plane = (long long)c.ny * c.nz;          // cells per x-plane (contiguous)
+  const size_t pbytes = (size_t)plane * nv * sizeof(double);
   cudaStream_t st = c.stage_stream;
-  if ((rc = cuda_status(cudaMemcpyAsync(c.d_stage_in, f_in_host, bytes, cudaMemcpyHostToDevice, st), "H2D"))) return rc;
-  if ((rc = fks_step(h, c.d_stage_in, c.d_stage_out, coll_scale, st))) return rc;
-  if ((rc = cuda_status(cudaMemcpyAsync(f_out_host, c.d_stage_out, bytes, cudaMemcpyDeviceToHost, st), "D2H"))) return rc;
-  return cuda_status(cudaStreamSynchronize(st), "host-buffer step");
+  const Shift sh = advance_generic_cell(c);
+  int dmax = 0;
+  for (int k = 0; k < c.N; k++) dmax = std::max(dmax, std::abs(sh.delta[0][k]));
+  const int nx = c.nx;
+  int nch = std::min(4, nx);                               // slabs
+  if (2 * dmax >= nx / nch) nch = 1;                       // halo too wide for slabs: one piece
+  std::vector<int> x0(nch + 1);
+  for (int i = 0; i <= nch; i++) x0[i] = (int)((long long)nx * i / nch);
+  const int wrap = (nch > 1) ? dmax : 0;                   // planes [nx - wrap, nx) go first
+  std::vector<cudaEvent_t> eh(nch), ec(nch);
+  for (int i = 0; i < nch; i++) {
+    cudaEventCreateWithFlags(&eh[i], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ec[i], cudaEventDisableTiming);
+  }
+  auto h2d = [&](int p0, int p1) -> fks_status {           // input planes [p0, p1)
+    if (p1 <= p0) return FKS_OK;
+    return cuda_status(cudaMemcpyAsync(c.d_stage_in + (size_t)p0 * plane * nv, f_in_host + (size_t)p0 * plane * nv,
+                                       (size_t)(p1 - p0) * pbytes, cudaMemcpyHostToDevice, c.h2d_stream), "H2D");
+  };
+  rc = h2d(nx - wrap, nx);
+  int copied = 0;                                          // planes [0, copied) are in flight
+  for (int i = 0; i < nch && !rc; i++) {
+    const int need = (i == nch - 1) ? nx - wrap : std::min(nx - wrap, x0[i + 1] + dmax);
+    if (!(rc = h2d(copied, need))) copied = std::max(copied, need);
+    if (!rc) rc = cuda_status(cudaEventRecord(eh[i], c.h2d_stream), "event");
+  }
+  const bool ident = shift_is_identity(sh);
+  for (int i = 0; i < nch && !rc; i++) {
+    const long long c0 = (long long)x0[i] * plane, m = (long long)(x0[i + 1] - x0[i]) * plane;
+    rc = cuda_status(cudaStreamWaitEvent(st, eh[i], 0), "wait H2D");
+    if (!rc) {
+      if (ident) rc = run_collision(c, c.d_stage_in + c0 * nv, c.d_stage_out + c0 * nv, m, true, coll_scale, st);
+      else {
+        rc = launch_transport_gather(c, c.d_stage_in, c.d_stage_out, sh, st, c0, m);
+        if (!rc) rc = run_collision(c, c.d_stage_out + c0 * nv, c.d_stage_out + c0 * nv, m, true, coll_scale, st);
+      }
+    }
+    if (!rc) rc = cuda_status(cudaEventRecord(ec[i], st), "event");
+    if (!rc) rc = cuda_status(cudaStreamWaitEvent(c.d2h_stream, ec[i], 0), "wait compute");
+    if (!rc) rc = cuda_status(cudaMemcpyAsync(f_out_host + c0 * nv, c.d_stage_out + c0 * nv, (size_t)m * nv * sizeof(double),
+                                              cudaMemcpyDeviceToHost, c.d2h_stream), "D2H");
+  }
+  fks_status rs = cuda_status(cudaStreamSynchronize(c.d2h_stream), "host-buffer step");
+  cudaStreamSynchronize(st);
+  cudaStreamSynchronize(c.h2d_stream);
+  for (int i = 0; i < nch; i++) { cudaEventDestroy(eh[i]); cudaEventDestroy(ec[i]); }
+  return rc ? rc : rs;
 }
 
 fks_status fks_get_info(const fks_ctx* h, int* P, int* T, double* R, double* lambda) {
@@ -485,6 +536,8 @@ void fks_destroy(fks_ctx* h) {
   if (c->d_stage_in) cudaFree(c->d_stage_in);
   if (c->d_stage_out) cudaFree(c->d_stage_out);
   if (c->stage_stream) cudaStreamDestroy(c->stage_stream);
+  if (c->h2d_stream) cudaStreamDestroy(c->h2d_stream);
+  if (c->d2h_stream) cudaStreamDestroy(c->d2h_stream);
   for (int ph = 0; ph < 4; ph++)
     for (auto& ev : c->prof.used[ph]) c->prof.pool.push_back(ev);
   for (auto& ev : c->prof.pool) { cudaEventDestroy(ev.first); cudaEventDestroy(ev.second); }

@@ -10,11 +10,11 @@ namespace fks {
 // 256/N at a time.  The source cell of every (axis, velocity index) is resolved once per CTA in shared memory
 // (no 64-bit division in the copy loop); a warp reads a few contiguous runs (one per distinct delta_z).
 __global__ void __launch_bounds__(256) transport_gather_kernel(const double* __restrict__ fin,
-                                                               double* __restrict__ fout, Shift sh) {
+                                                               double* __restrict__ fout, Shift sh, long long cell0) {
   __shared__ int sx[kMaxN], sy[kMaxN], sz[kMaxN];
   const int N = sh.N;
   const long long nv = (long long)N * N * N;
-  const long long j = blockIdx.x;
+  const long long j = cell0 + blockIdx.x;
   const int jz = (int)(j % sh.nz), jy = (int)((j / sh.nz) % sh.ny);
   const int jx = (int)(j / ((long long)sh.nz * sh.ny));
   if (threadIdx.x < N) {
@@ -38,11 +38,13 @@ __global__ void __launch_bounds__(256) transport_gather_kernel(const double* __r
   }
 }
 
-fks_status launch_transport_gather(Ctx& c, const double* fin, double* fout, const Shift& sh, cudaStream_t st) {
+fks_status launch_transport_gather(Ctx& c, const double* fin, double* fout, const Shift& sh, cudaStream_t st,
+                                   long long cell0, long long ncells) {
   const long long cells = (long long)sh.nx * sh.ny * sh.nz;
-  if (cells == 0) return FKS_OK;
-  if (cells > 0x7fffffffLL) { set_error("transport: too many cells"); return FKS_ERR_INVALID; }
-  transport_gather_kernel<<<(unsigned)cells, 256, 0, st>>>(fin, fout, sh);
+  if (ncells < 0) ncells = cells - cell0;  // destination cells [cell0, cell0 + ncells); sources anywhere in fin
+  if (ncells <= 0) return FKS_OK;
+  if (ncells > 0x7fffffffLL) { set_error("transport: too many cells"); return FKS_ERR_INVALID; }
+  transport_gather_kernel<<<(unsigned)ncells, 256, 0, st>>>(fin, fout, sh, cell0);
   c.launches++;
   return cuda_status(cudaPeekAtLastError(), "transport gather");
 }

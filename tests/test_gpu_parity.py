@@ -282,3 +282,46 @@ def test_c4_full_box_step_sampled(cuda_device):
         assert abs(m1 - m0) / abs(m0) <= 1e-12
         cur, nxt = nxt, cur
     del f, g
+
+
+# ---------------- host-buffer step: slab-pipelined copies must not change a single bit ----------------------
+
+@pytest.mark.parametrize("name,shape,cfl", [("c2", (16, 2, 1), (1, 1)), ("c2", (12, 1, 2), (3, 1)), ("c0", (5, 2, 1), (1, 2))])
+def test_step_host_matches_device(cuda_device, name, shape, cfl):
+    """fks_step_host (pinned host buffers, 3-stream slab pipeline with a periodic halo of max|delta_x| planes)
+    equals fks_step on device buffers bit for bit, over two consecutive steps (the generic cell advances)."""
+    cfg = CONFIGS[name]
+    n = shape[0] * shape[1] * shape[2]
+    f = inputs.make_f(cfg, device=cuda_device, cells=[i % cfg.n_cells for i in range(n)])
+    dev = make(cfg)
+    host = make(cfg)
+    dev.transport_setup(shape, *cfl)
+    host.transport_setup(shape, *cfl)
+    a, b = f.clone(), torch.empty_like(f)
+    ha = torch.empty(f.shape, dtype=torch.float64, pin_memory=True)
+    hb = torch.empty_like(ha, pin_memory=True)
+    ha.copy_(f)
+    for _ in range(2):
+        dev.step(a, b, 0.01)
+        B.fks_step_host(host.h, ha, hb, 0.01)
+        a, b = b, a
+        ha, hb = hb, ha
+    torch.cuda.synchronize()
+    assert torch.equal(a.cpu(), ha)
+
+
+def test_step_host_pageable(cuda_device):
+    """Pageable host memory takes the same path (copies become synchronous) and gives the same bits."""
+    cfg = CONFIGS["c2"]
+    shape = (8, 1, 1)
+    f = inputs.make_f(cfg, device=cuda_device, cells=list(range(8)))
+    dev, host = make(cfg), make(cfg)
+    dev.transport_setup(shape, 1, 1)
+    host.transport_setup(shape, 1, 1)
+    out = torch.empty_like(f)
+    dev.step(f, out, 0.02)
+    hin = f.cpu().contiguous()
+    hout = torch.empty_like(hin)
+    B.fks_step_host(host.h, hin, hout, 0.02)
+    torch.cuda.synchronize()
+    assert torch.equal(out.cpu(), hout)
