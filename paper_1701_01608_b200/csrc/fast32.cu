@@ -664,6 +664,10 @@ constexpr int NB = 4;                         // W1 team buffers (Z warps run ah
 #ifndef V4_G4
 #define V4_G4 1
 #endif
+// V4_XP = 1 (with G6): X warps park their rows in TMEM and run all three px classes from there
+#ifndef V4_XP
+#define V4_XP 1
+#endif
 #if V4_G6
 constexpr int GW = 6;                         // warps per YX group
 #ifndef V4_NZW
@@ -851,6 +855,15 @@ __device__ __forceinline__ void xform48x2s(const double2* b1, const double2* b2,
   fftd::fft16<1>(v);
 }
 
+__device__ __forceinline__ void tmem_ld16_async(uint32_t addr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(addr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
 __device__ __forceinline__ void g_accumulate(uint32_t tcol, const double2 (&u)[16]) {
   uint32_t gw[32];
   tmem_ld32(tcol, gw);
@@ -884,8 +897,13 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
   const long long total_tg = ncell_team * A.T1;
 
   if (warp == 0) {
+#if V4_G6 && V4_XP
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;"
+                 ::"r"((uint32_t)__cvta_generic_to_shared(&tmem_base_sh)));
+#else
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;"
                  ::"r"((uint32_t)__cvta_generic_to_shared(&tmem_base_sh)));
+#endif
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
@@ -903,6 +921,182 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
   const uint32_t tbase = tmem_base_sh;
 
   if (warp < NYX) {
+#if V4_G6 && V4_XP
+    // --------------------------------- YX warps, X rows parked in TMEM -------------------------------------
+    // 6 X warps (one per group and row class c; warps 0..5 -> (g,c) = (0,0) (0,1) (0,2) (1,2) (1,0) (1,1), lane
+    // quarters 0,1,2,3,0,1) and 6 Y warps (6..11 -> (g, c) = (w-6)/3, (w-6)%3).  Per term t:
+    //   Y(g,c): wait W1(t) and slot c free (X(g,c) parked term t-1); class c of the y-pass of both planes
+    //           -> slot c; count yc[g][c] = t+1; the last Y warp of the group done with W1(t) prefetches W1(t+1).
+    //   X(g,c): wait yc[g][c] = t+1; load its 32 rows of class c once, park them in TMEM (124 columns), free the
+    //           slot (xc[g][c] = t+1), then the three px classes from TMEM with G += Re z Im z (3 x 32 columns).
+    const bool isx = warp < 6;
+    const int g = isx ? ((warp >= 3) ? 1 : 0) : (warp - 6) / 3;
+    const int c = isx ? (warp < 3 ? warp : (warp == 3 ? 2 : warp - 4)) : (warp - 6) % 3;
+    double2* pb0 = reinterpret_cast<double2*>(smem + (2 * g) * PLANE_B);
+    double2* pb1 = reinterpret_cast<double2*>(smem + (2 * g + 1) * PLANE_B);
+    double2* in0 = pb0;
+    double2* in1 = pb1;
+    auto ybuf = [&](int pl, int slot) { return (pl ? pb1 : pb0) + NPEN + slot * YB; };
+    const int pz0 = PLN * k + 2 * g;
+    const uint32_t tX = tbase + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(warp >= 4 && warp < 6 ? 224 : 0);
+    const uint32_t tPark = tX + 96u;
+    const int xp = lane >> 4, xq = lane & 15;
+    int* yc = s_yc[g];
+    int* xc = s_xc[g];
+    auto wait_ge = [&](const int* ptr, int target) {
+      if (lane == 0) {
+        long long spins = 0;
+        unsigned ns = 32;
+        while (vload(ptr) < target) {
+          __nanosleep(ns);
+          if (ns < 512) ns <<= 1;
+          if (++spins > (1LL << 26)) asm volatile("trap;");
+        }
+      }
+      __syncwarp();
+    };
+    auto issue_w1 = [&](long long tgi) {
+      const double2* src = W1t + (tgi % NB) * (long long)W1_BUF + (long long)pz0 * NPEN;
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_expect(&bar_w1[g], 2u * W1IN_B);
+      bulk_g2s(in0, src, W1IN_B, &bar_w1[g]);
+      bulk_g2s(in1, src + NPEN, W1IN_B, &bar_w1[g]);
+    };
+    auto try_issue_w1 = [&](long long tz, bool block) {  // lane 0: bulk-copy W1(tz) once per group
+      if (tz >= total_tg) return;
+      if (vload(&s_w1iss[g]) > (int)tz) return;
+      if (vload(&s_yall[g]) < 3 * (int)tz) {
+        if (!block) return;
+        long long spins = 0;
+        while (vload(&s_yall[g]) < 3 * (int)tz) { __nanosleep(64); if (++spins > (1LL << 26)) asm volatile("trap;"); }
+      }
+      unsigned* zc = zcnt + 32 * (tz % NB);
+      const unsigned target = (unsigned)(TM * (tz / NB + 1));
+      if (block) poll_ge(zc, target);
+      else if (ld_acquire(zc) < target) return;
+      if (atomicCAS(&s_w1iss[g], (int)tz, (int)tz + 1) == (int)tz) issue_w1(tz);
+    };
+    uint32_t par = 0;
+    long long tg = 0;
+#pragma unroll 1
+    for (long long cell = team; cell < A.n_cells; cell += A.nteams) {
+#pragma unroll 1
+      for (int t = 0; t < A.T1; t++, tg++) {
+        const int T = (int)tg;
+        long long* st = (A.dbg && lane == 0 && warp == 6 && cell == team && t >= 2 && t < 6)
+                            ? A.dbg + (long long)blockIdx.x * 128 + (t - 2) * 16 : nullptr;
+        if (st) st[0] = clock64();
+        if (!isx) {
+          // ---------------- Y warp ----------------
+          if (lane == 0 && c == 0) try_issue_w1(tg, true);
+          mbar_wait(&bar_w1[g], par);
+          if (c == 0 && lane == 0) {
+            __threadfence();
+            atomicAdd(ycnt + 32 * (tg % NB), 1u);  // this group has consumed W1(tg)
+          }
+          if (st) st[1] = clock64();
+          wait_ge(&xc[c], T);  // slot c: X(g, c) of term t-1 has parked its rows
+#pragma unroll 1
+          for (int pl = 0; pl < 2; pl++) {
+            double2 u[16];
+            xform48((pl ? in1 : in0) + (lane < K ? lane : K - 1) * K, 1, c, u);
+            if (lane < K) {
+              double2* ydst = ybuf(pl, c) + lane;
+#pragma unroll
+              for (int q = 0; q < 16; q++) ydst[q * K] = u[fftd::qslot(q)];
+            }
+          }
+          __syncwarp();
+          if (lane == 0) {
+            __threadfence_block();
+            atomicAdd(&yc[c], 1);
+            if (atomicAdd(&s_yall[g], 1) + 1 == 3 * (T + 1)) try_issue_w1(tg + 1, false);  // prefetch
+          }
+          if (st) st[2] = clock64();
+        } else {
+          // ---------------- X warp ----------------
+          wait_ge(&yc[c], T + 1);
+          if (t == 0) {  // first term of the cell: zero the three G blocks
+            uint32_t zw[32];
+#pragma unroll
+            for (int i = 0; i < 32; i++) zw[i] = 0u;
+#pragma unroll 1
+            for (int rx = 0; rx < 3; rx++) tmem_st32(tX + 32u * rx, zw);
+          }
+          {  // park the row (31 complex = 124 words) in this lane's TMEM columns, 8 values per store
+            const double2* row = ybuf(xp, c) + xq * K;
+#pragma unroll
+            for (int ch = 0; ch < 4; ch++) {
+              uint32_t w[32];
+#pragma unroll
+              for (int k2 = 0; k2 < 8; k2++) {
+                const int i = 8 * ch + k2;
+                const double2 v = (i < K) ? row[i] : make_double2(0.0, 0.0);
+                w[4 * k2] = (uint32_t)__double2loint(v.x);
+                w[4 * k2 + 1] = (uint32_t)__double2hiint(v.x);
+                w[4 * k2 + 2] = (uint32_t)__double2loint(v.y);
+                w[4 * k2 + 3] = (uint32_t)__double2hiint(v.y);
+              }
+              tmem_st32(tPark + 32u * ch, w);
+            }
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+          }
+          __syncwarp();
+          if (lane == 0) {
+            __threadfence_block();
+            atomicAdd(&xc[c], 1);  // the Y slot may be refilled
+          }
+#pragma unroll 1
+          for (int rx = 0; rx < 3; rx++) {
+            double2 u[16];
+            const double sg = (rx == 1) ? -0.86602540378443864676 : 0.86602540378443864676;
+#pragma unroll
+            for (int mm = 0; mm < 4; mm++) {  // x[4mm..4mm+3] (a) and x[16+4mm..19+4mm] (b) -> u[4mm+1..4mm+4]
+              uint32_t wa[16], wb[16];
+              tmem_ld16_async(tPark + 16u * mm, wa);
+              tmem_ld16_async(tPark + 64u + 16u * mm, wb);
+              tmem_wait_ld();
+#pragma unroll
+              for (int k2 = 0; k2 < 4; k2++) {
+                const int m = 4 * mm + k2 + 1;
+                const double2 va = make_double2(__hiloint2double((int)wa[4 * k2 + 1], (int)wa[4 * k2]),
+                                                __hiloint2double((int)wa[4 * k2 + 3], (int)wa[4 * k2 + 2]));
+                if (mm == 3 && k2 == 3) { u[0] = va; continue; }  // x[15]
+                const double2 vb = make_double2(__hiloint2double((int)wb[4 * k2 + 1], (int)wb[4 * k2]),
+                                                __hiloint2double((int)wb[4 * k2 + 3], (int)wb[4 * k2 + 2]));
+                if (rx == 0) {
+                  u[m] = fftd::cadd(vb, va);
+                } else {
+                  double2 acc;
+                  acc.x = fma(-0.5, va.x, vb.x);
+                  acc.x = fma(-sg, va.y, acc.x);
+                  acc.y = fma(-0.5, va.y, vb.y);
+                  acc.y = fma(sg, va.x, acc.y);
+                  u[m] = fftd::cmul_s<1>(fftd::c_tw48[rx * m], acc);
+                }
+              }
+            }
+            fftd::fft16<1>(u);
+            g_accumulate(tX + 32u * rx, u);
+          }
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+          if (t == A.T1 - 1) {  // G[cell][px = 3q' + rx][pz][py = 3 xq + c]
+            double* Gc = A.G + cell * (long long)(P * P * P) + (long long)(pz0 + xp) * P;
+#pragma unroll 1
+            for (int rx = 0; rx < 3; rx++) {
+              uint32_t gw[32];
+              tmem_ld32(tX + 32u * rx, gw);
+#pragma unroll
+              for (int q = 0; q < 16; q++)
+                Gc[(long long)(3 * q + rx) * P * P + 3 * xq + c] = __hiloint2double((int)gw[2 * q + 1], (int)gw[2 * q]);
+            }
+          }
+        }
+        par ^= 1;
+      }
+    }
+#else
     // ---------------------------------------------- YX warps ----------------------------------------------
     const int g = warp / GW, wr = warp - GW * (warp / GW);
     double2* pb0 = reinterpret_cast<double2*>(smem + (2 * g) * PLANE_B);
@@ -1154,6 +1348,7 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
 #endif
       }
     }
+#endif
   } else {
     // ---------------------------------------------- Z warps -----------------------------------------------
     const int zt = tid - 32 * NYX;  // 0..NZT-1
@@ -1234,6 +1429,7 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
           const int na = nh + nmir;
 #pragma unroll 1
           for (int kk = zt; kk < 2 * NZT; kk += NZT) {
+            if (kk - lane >= 3 * na) break;  // no active lane in this warp (warp-uniform)
             const bool act = kk < 3 * na;
             const int kc = act ? kk : 0;
             const int r = kc / na, j = kc - r * na;
@@ -1283,7 +1479,11 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+#if V4_G6 && V4_XP
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tbase));
+#else
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tbase));
+#endif
 }
 }  // namespace v4
 

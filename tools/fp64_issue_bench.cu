@@ -3,7 +3,7 @@
 #include <cstdio>
 #include <cuda_runtime.h>
 
-template <int ILP, bool ADD>
+template <int ILP, int OP>  // OP 0 DFMA, 1 DADD, 2 DMUL
 __global__ void chains(double* out, int iters, double a, double b) {
   double x[ILP];
 #pragma unroll
@@ -11,7 +11,7 @@ __global__ void chains(double* out, int iters, double a, double b) {
   long long t0 = clock64();
   for (int it = 0; it < iters; it++) {
 #pragma unroll
-    for (int i = 0; i < ILP; i++) x[i] = ADD ? x[i] + a : fma(x[i], a, b);
+    for (int i = 0; i < ILP; i++) x[i] = OP == 1 ? x[i] + a : (OP == 2 ? x[i] * a : fma(x[i], a, b));
   }
   long long t1 = clock64();
   double s = 0;
@@ -21,12 +21,12 @@ __global__ void chains(double* out, int iters, double a, double b) {
   if (threadIdx.x == 0) ((long long*)out)[1 + blockIdx.x] = t1 - t0;
 }
 
-template <int ILP, bool ADD>
+template <int ILP, int OP>
 void run(int warps, int sms, double* out) {
   const int iters = 4096;
-  chains<ILP, ADD><<<sms, warps * 32>>>(out, 64, 1.0000001, 1e-9);
+  chains<ILP, OP><<<sms, warps * 32>>>(out, 64, 1.0000001, 1e-9);
   cudaDeviceSynchronize();
-  chains<ILP, ADD><<<sms, warps * 32>>>(out, iters, 1.0000001, 1e-9);
+  chains<ILP, OP><<<sms, warps * 32>>>(out, iters, 1.0000001, 1e-9);
   cudaDeviceSynchronize();
   long long cyc[256];
   cudaMemcpy(cyc, out + 1, sizeof(long long) * sms, cudaMemcpyDeviceToHost);
@@ -34,24 +34,18 @@ void run(int warps, int sms, double* out) {
   for (int i = 0; i < sms; i++) mx = cyc[i] > mx ? cyc[i] : mx;
   const double ops = (double)iters * ILP * warps * 32;
   printf("{\"op\": \"%s\", \"warps_per_sm\": %d, \"ilp\": %d, \"lane_ops_per_clk_sm\": %.2f, \"clk_per_dependent_op\": %.2f}\n",
-         ADD ? "dadd" : "dfma", warps, ILP, ops / mx, (double)mx / iters);
+         OP == 1 ? "dadd" : (OP == 2 ? "dmul" : "dfma"), warps, ILP, ops / mx, (double)mx / iters);
 }
 
 int main() {
   double* out;
   cudaMalloc(&out, 4096 * sizeof(double));
   int sms = 148;
-  for (int w : {1, 2, 4, 8, 12, 16}) {
-    run<1, false>(w, sms, out);
-    run<2, false>(w, sms, out);
-    run<4, false>(w, sms, out);
-    run<8, false>(w, sms, out);
-    run<16, false>(w, sms, out);
-  }
-  for (int w : {4, 8}) {
-    run<1, true>(w, sms, out);
-    run<4, true>(w, sms, out);
-    run<8, true>(w, sms, out);
+  for (int w : {8, 16, 32}) {
+    run<8, 0>(w, sms, out);
+    run<8, 1>(w, sms, out);
+    run<8, 2>(w, sms, out);
+    run<4, 1>(w, sms, out);
   }
   return 0;
 }
