@@ -1416,7 +1416,13 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
         }
         nbar(3, NZT);  // products complete (after the cell's last term the f^ block is free)
         if (zt == 0 && t == A.T1 - 1 && cell + A.nteams < A.n_cells) issue_fh(cell + A.nteams);
-        if (zt == 0 && tg > 0) red_release_add(zcnt + 32 * ((tg - 1) % NB), 1u);  // publish W1(tg - 1)
+        // publish W1(tg - 2) and W1(tg - 1) every second term: one store drain per pair (it costs ~1.4 K cycles
+        // on the Z warps, which set the period; the consumers have slack)
+        if (zt == 0 && tg >= 2 && (tg & 1) == 0) {
+          __threadfence();
+          atomicAdd(zcnt + 32 * ((tg - 2) % NB), 1u);
+          atomicAdd(zcnt + 32 * ((tg - 1) % NB), 1u);
+        }
         if (st) st[2] = clock64();
         if (zt == 0) {
           if (tg >= NB) poll_ge(ycnt + 32 * (tg % NB), (unsigned)(2 * TM * (tg / NB)));  // buffer free
@@ -1475,7 +1481,11 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
         if (st) st[4] = clock64();
       }
     }
-    if (zt == 0 && tg > 0) red_release_add(zcnt + 32 * ((tg - 1) % NB), 1u);  // publish the last term
+    if (zt == 0 && tg > 0) {  // publish what is left (tg even: W1(tg-2), W1(tg-1); tg odd: W1(tg-1))
+      __threadfence();
+      if ((tg & 1) == 0 && tg >= 2) atomicAdd(zcnt + 32 * ((tg - 2) % NB), 1u);
+      atomicAdd(zcnt + 32 * ((tg - 1) % NB), 1u);
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
