@@ -243,7 +243,7 @@ def main():
     # DRAM traffic of the dominant kernel from the committed ncu --set full capture (per cell, scaled to this
     # run's cells per launch); null when no capture of the current kernel is committed
     traffic = None
-    tpath = os.path.join(ROOT, "profiles", "r01h_hot_kernel_traffic.json")
+    tpath = os.path.join(ROOT, "profiles", "r01i_hot_kernel_traffic.json")
     if os.path.exists(tpath) and col.info.get("path") == 2:
         try:
             tj = json.load(open(tpath))
@@ -282,7 +282,7 @@ def main():
         "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": workload,
         "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "traffic_note": "dram__bytes_read+write per launch from profiles/r01h_hot_kernel_traffic.json "
+                     "traffic_note": "dram__bytes_read+write per launch from profiles/r01i_hot_kernel_traffic.json "
                                      "(ncu --set full of this kernel in this bench command), scaled to cells per launch",
                      "kernel": "term loop (a3-a5: table product, pruned 3D inverse, gain-loss accumulate)",
                      "flop_per_cell": fl["hot"], "cells_per_launch": cells_per_launch, "ms_per_launch": hot_ms,
