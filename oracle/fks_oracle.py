@@ -501,3 +501,82 @@ def velocity_grid3(N: int, L: float) -> np.ndarray:
     v = velocity_nodes(N, L)
     X, Y, Z = np.meshgrid(v, v, v, indexing="ij")
     return np.stack([X, Y, Z], axis=-1)
+
+
+# ---------------------------------------------------------------------------------------------------
+# Macroscopic moments (ToConservative / ToPrimitive) and the BGK operator
+# ---------------------------------------------------------------------------------------------------
+
+def collision_invariants(N: int, L: float) -> np.ndarray:
+    """φ(v_k) = (1, v_x, v_y, v_z, |v|²/2) at every node: shape (5, N, N, N)."""
+    v3 = velocity_grid3(N, L)
+    return np.stack([np.ones(v3.shape[:-1]), v3[..., 0], v3[..., 1], v3[..., 2], 0.5 * np.sum(v3 * v3, axis=-1)])
+
+
+def moments(f: np.ndarray, N: int, L: float) -> np.ndarray:
+    """ToConservative: U_j = Σ_k φ(v_k) f_{j,k} (Δv)³ = (ρ, ρu_x, ρu_y, ρu_z, E) per cell.
+
+    f: (n_cells, N, N, N) or (N, N, N); Δv = 2L/N.  Returns (n_cells, 5) or (5,)."""
+    h3 = (2.0 * L / N) ** 3
+    phi = collision_invariants(N, L)
+    fc = f.reshape(-1, N, N, N)
+    U = np.array([[np.sum(phi[a] * fc[c]) * h3 for a in range(5)] for c in range(fc.shape[0])])
+    return U if f.ndim > 3 else U[0]
+
+
+def moments_update(U_prev: np.ndarray, f_prev: np.ndarray, shape, delta: np.ndarray, N: int, L: float) -> np.ndarray:
+    """Eq. DM_update: U_j^{n+1} = U_j^n + Σ_{k moved} (m_{j−δ(k),k} − m_{j,k}) φ(v_k) (Δv)³.
+
+    Only the particles that change cell contribute (δ(k) ≠ 0); written as the paper's sum over particles."""
+    h3 = (2.0 * L / N) ** 3
+    phi = collision_invariants(N, L)
+    U = np.array(U_prev, dtype=np.float64, copy=True)
+    n = f_prev.shape[0]
+    for j in range(n):
+        src = source_cells(j, shape, delta)
+        for kx in range(N):
+            for ky in range(N):
+                for kz in range(N):
+                    if delta[0, kx] == 0 and delta[1, ky] == 0 and delta[2, kz] == 0:
+                        continue
+                    dm = f_prev[src[kx, ky, kz], kx, ky, kz] - f_prev[j, kx, ky, kz]
+                    U[j] += dm * phi[:, kx, ky, kz] * h3
+    return U
+
+
+def primitive(U: np.ndarray) -> np.ndarray:
+    """ToPrimitive: (ρ, u, T) from (ρ, ρu, E) with (3/2)ρT = E − ρ|u|²/2.  Shape (..., 5)."""
+    U = np.asarray(U, dtype=np.float64)
+    rho = U[..., 0]
+    with np.errstate(divide="ignore", invalid="ignore"):
+        u = U[..., 1:4] / rho[..., None]
+        T = (U[..., 4] - 0.5 * rho * np.sum(u * u, axis=-1)) / (1.5 * rho)
+    return np.concatenate([rho[..., None], u, T[..., None]], axis=-1)
+
+
+def local_maxwellian(f: np.ndarray, N: int, L: float) -> np.ndarray:
+    """E_{j,k} = M[f_j](v_k): the Maxwellian with the cell's (ρ, u, T) sampled at the nodes (P:179-183,
+    P:397-410).  Reading A26: a cell with ρ ≤ 0 or T ≤ 0 (no Maxwellian exists) gets E = 0."""
+    fc = f.reshape(-1, N, N, N)
+    W = primitive(moments(fc, N, L).reshape(-1, 5))
+    v3 = velocity_grid3(N, L)
+    E = np.zeros_like(fc)
+    for c in range(fc.shape[0]):
+        rho, u, T = W[c, 0], W[c, 1:4], W[c, 4]
+        if rho > 0 and T > 0:
+            E[c] = maxwellian(v3, rho, u, T)
+    return E.reshape(f.shape)
+
+
+def bgk(f: np.ndarray, N: int, L: float, nu: float) -> np.ndarray:
+    """Q_BGK(f) = ν (M[f] − f) per cell."""
+    return nu * (local_maxwellian(f, N, L) - f)
+
+
+def bgk_step(f: np.ndarray, shape, cell: GenericCell, nu_dt: float, L: float) -> np.ndarray:
+    """One FKS step with the BGK operator: transport, then explicit Euler f^{n+1} = f* + Δt ν (E − f*)
+    (Eq. disc_relax; A17).  nu_dt = ν Δt."""
+    N = f.shape[-1]
+    delta = cell.advance()
+    fs = transport(f, shape, delta)
+    return fs + nu_dt * (local_maxwellian(fs, N, L) - fs)
