@@ -135,6 +135,161 @@ def time_oracle(cfg, budget_s: float, max_cells: int = 256) -> dict:
 
 
 # ------------------------------------------------------------------------------------------------------
+# BGK workload: fks_bgk_step = transport gather + moments + BGK relaxation, one fused
+# kernel; HBM-bound (algorithmic traffic 16 B per cell-velocity point: read f_in once, write f_out once)
+# ------------------------------------------------------------------------------------------------------
+
+BGK_NU = 10.0  # ν = 1/τ with τ = 0.1, the paper's BGK Sod runs
+
+
+def hbm_peak_gbs() -> tuple:
+    try:
+        return float(json.load(open(MEASURED_PEAKS))["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (copy, burst)"
+    except Exception:
+        return 7700.0, "nominal 7.7 TB/s (MEASURED_PEAKS.json unavailable)"
+
+
+def time_oracle_bgk(cfg, budget_s: float, nu_dt: float, max_cells: int = 1024) -> dict:
+    import numpy as np  # noqa: F401
+    from oracle import fks_oracle as o
+    from paper_1701_01608_b200 import inputs
+    cells = inputs.sample_cells(cfg, min(max_cells, cfg.n_cells), seed=7)
+    f = inputs.make_f(cfg, cells=cells).numpy()
+    t0 = time.perf_counter()
+    n = 0
+    for fc in f:  # transport is a permutation of the inputs: relaxation of the sampled cells
+        fc + nu_dt * (o.local_maxwellian(fc, cfg.N, cfg.L) - fc)
+        n += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    dt = time.perf_counter() - t0
+    return {"cells": n, "seconds": dt, "value": n * cfg.N ** 3 / dt}
+
+
+def bgk_traffic(cfg):
+    try:
+        tj = json.load(open(os.path.join(ROOT, "profiles", "r01j_bgk_step_traffic.json")))
+        return tj["dram_bytes_per_cell"] * cfg.n_cells if cfg.N == 32 else None
+    except Exception:
+        return None
+
+
+def run_bgk(args):
+    from paper_1701_01608_b200 import dist as D
+    from paper_1701_01608_b200.configs import CONFIGS
+    cfg = CONFIGS[args.config]
+    ws, rank, local = D.world()
+    metric = "fp64 BGK FKS step (transport + moments + relaxation) cell·velocity-points/s; fraction of HBM roofline"
+    unit = "cell·vp/s"
+    dt_over_dx = cfg.cfl_num / cfg.cfl_den / cfg.L  # Δt = c Δx / L
+    nu_dt = BGK_NU * dt_over_dx / cfg.shape[0]
+    workload = {"workload": f"{cfg.name} box, BGK operator: {cfg.shape[0]}x{cfg.shape[1]}x{cfg.shape[2]} cells x "
+                            f"{cfg.N}^3 velocities, fks_bgk_step (transport c={cfg.cfl_num}/{cfg.cfl_den}, "
+                            f"nu={BGK_NU}, nu*dt={nu_dt:.6g})",
+                "config": cfg.name, "n_cells": cfg.n_cells, "N": cfg.N,
+                "l2": "inputs larger than L2 (f is %.2f GB per copy)" % (cfg.n_cells * cfg.N ** 3 * 8 / 1e9)}
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        times, cells = [], 0
+        per_step = max(2.0, min(args.cpu_seconds, 120.0 / max(1, args.steps + args.warmup)))
+        for i in range(args.warmup + args.steps):
+            r = time_oracle_bgk(cfg, per_step, nu_dt)
+            if i >= args.warmup:
+                times.append(r["seconds"])
+                cells += r["cells"]
+        val = cells * cfg.N ** 3 / sum(times)
+        print(json.dumps({"impl": "reference", "metric": metric, "value": val, "unit": unit, "n_gpus": args.gpus,
+                          "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
+                          "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                          "data": "synthetic", "config": workload,
+                          "cpu_baseline": {"value": val, "unit": unit, "cores": oracle_threads(), "kind": "oracle",
+                                           "sample": f"{cells} cells of {cfg.name} (BGK relaxation per sampled cell)"},
+                          "e2e": {"value": val, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_1701_01608_b200 import binding as B
+    from paper_1701_01608_b200 import inputs
+    if ws > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", init_method="env://")
+    dev = torch.device("cuda", local if ws > 1 else 0)
+    torch.cuda.set_device(dev)
+    stream = torch.cuda.current_stream(dev)
+    col = B.Collision(cfg.N, cfg.L, cfg.M, cfg.M_r, cfg.kernel)
+    fa = inputs.make_f(cfg, device=dev, seed=D.rank_seed(rank))
+    fb = torch.empty_like(fa)
+    col.transport_setup(cfg.shape, cfg.cfl_num, cfg.cfl_den)
+
+    def barrier():
+        if ws > 1:
+            dist.barrier()
+
+    bufs = [fa, fb]
+    for i in range(args.warmup):
+        col.bgk_step(bufs[i % 2], bufs[(i + 1) % 2], nu_dt)
+    torch.cuda.synchronize()
+    barrier()
+    n0 = col.launches()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev.index or 0) as clk:
+        torch.cuda.synchronize()
+        barrier()
+        e0.record(stream)
+        for i in range(args.steps):
+            col.bgk_step(bufs[(args.warmup + i) % 2], bufs[(args.warmup + i + 1) % 2], nu_dt)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    launches = col.launches() - n0
+    ms_step = D.max_over_ranks(e0.elapsed_time(e1), dev) / args.steps
+    value = D.weak_value(cfg.n_cells, cfg.N ** 3, ws, ms_step)
+    nbytes = cfg.n_cells * cfg.N ** 3 * 8
+    achieved = 2 * nbytes / (ms_step / 1e3) / 1e9
+    peak, peak_note = hbm_peak_gbs()
+
+    e2e = None
+    if not args.no_e2e:  # pinned host -> device, the fused step, device -> pinned host, all timed
+        hin = torch.empty(fa.shape, dtype=torch.float64, pin_memory=True)
+        hout = torch.empty_like(hin, pin_memory=True)
+        hin.copy_(fa)
+        torch.cuda.synchronize()
+        barrier()
+        t0 = time.perf_counter()
+        for i in range(args.e2e_steps):
+            fa.copy_(hin, non_blocking=True)
+            col.bgk_step(fa, fb, nu_dt)
+            hout.copy_(fb, non_blocking=True)
+        torch.cuda.synchronize()
+        dt = D.max_over_ranks(time.perf_counter() - t0, dev)
+        e2e = {"value": cfg.n_cells * ws * cfg.N ** 3 * args.e2e_steps / dt, "unit": unit,
+               "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes, "steps": args.e2e_steps,
+               "api": "torch pinned H2D + Collision.bgk_step (fks_bgk_step) + D2H"}
+        del hin, hout
+    if rank != 0:
+        if ws > 1:
+            dist.destroy_process_group()
+        return
+    cpu = time_oracle_bgk(cfg, min(args.cpu_seconds, 10.0), nu_dt)
+    print(json.dumps({
+        "metric": metric, "value": value, "unit": unit, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": workload,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": bgk_traffic(cfg),
+                     "traffic_note": "dram__bytes_read+write per launch from profiles/r01j_bgk_step_traffic.json "
+                                     "(ncu --set full of this kernel on this workload)",
+                     "kernel": "macro_kernel<BGK_STEP> (fused transport gather + moments + relaxation)",
+                     "bytes_per_cell_vp": 16, "peak_note": peak_note},
+        "clocks": clk.summary(), "gpu_launches": launches, "e2e": e2e,
+        "cpu_baseline": {"value": cpu["value"], "unit": unit, "cores": oracle_threads(), "kind": "oracle",
+                         "sample": f"{cpu['cells']} sampled cells of {cfg.name}, BGK relaxation, {cpu['seconds']:.1f} s"},
+    }))
+    if ws > 1:
+        dist.destroy_process_group()
+
 
 def main():
     ap = argparse.ArgumentParser()
@@ -146,7 +301,11 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--workload", default="boltzmann", choices=["boltzmann", "bgk"],
+                    help="bgk: the BGK-operator FKS step (SURVEY §8(f) NEXT-3; HBM-bound) on the same config")
     args = ap.parse_args()
+    if args.workload == "bgk":
+        return run_bgk(args)
 
     from paper_1701_01608_b200 import dist as D
     from paper_1701_01608_b200.configs import CONFIGS

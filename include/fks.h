@@ -102,6 +102,25 @@ fks_status fks_step(fks_ctx* h, const double* f_in, double* f_out, double coll_s
 /* Host-buffer variant of fks_step (synchronous), for the end-to-end measurement. */
 fks_status fks_step_host(fks_ctx* h, const double* f_in_host, double* f_out_host, double coll_scale);
 
+/* Macroscopic moments per cell ("ToConservative" / "ToPrimitive"):
+ *   U[c] = sum_k phi(v_k) f[c][k] dv^3 = (rho, rho u_x, rho u_y, rho u_z, E),  phi = (1, v, |v|^2/2), dv = 2L/N;
+ *   W[c] = (rho, u_x, u_y, u_z, T) with (3/2) rho T = E - rho |u|^2 / 2.
+ * U and W are DEVICE arrays [n_cells][5] fp64; either may be NULL (not both).  rho = 0 gives non-finite u, T.
+ * Direct sums (the paper's incremental Eq. DM_update gives the same numbers after transport, pin P20). */
+fks_status fks_moments(fks_ctx* h, const double* f, double* U, double* W, long long n_cells, void* stream);
+
+/* BGK operator: Q[c] = nu (E[f[c]] - f[c]), E the Maxwellian with f[c]'s (rho, u, T)
+ * sampled at the velocity nodes; E = 0 for a cell with rho <= 0 or T <= 0 (A26).  Q must not overlap f. */
+fks_status fks_bgk_batch(fks_ctx* h, const double* f, double* Q, double nu, long long n_cells, void* stream);
+
+/* One FKS time step with the BGK operator (Eq. disc_relax): transport (as
+ * fks_transport_step, requires fks_transport_setup; advances the generic cell), then explicit Euler
+ * f_out = f* + nu_dt (E[f*] - f*), nu_dt = nu * dt.  One fused kernel: f_in is read once and f_out written
+ * once.  Optional U, W ([n_cells][5], device, may be NULL) receive the moments of the transported f*
+ * (the relaxation keeps them up to the velocity-grid quadrature error, P18/P22). */
+fks_status fks_bgk_step(fks_ctx* h, const double* f_in, double* f_out, double nu_dt, double* U, double* W,
+                        void* stream);
+
 /* Diagnostics: padded size P, number of separated terms T (the loss term t = 0 is extra), cutoff R_c,
  * lambda = 2/(3+sqrt 2).  Any out pointer may be NULL. */
 fks_status fks_get_info(const fks_ctx* h, int* P, int* T, double* R, double* lambda);

@@ -24,7 +24,7 @@ EXPORTS = ["fks_collision_init", "fks_collision_init_ex", "fks_collision_batch",
            "fks_transport_setup", "fks_transport_step", "fks_step", "fks_step_host", "fks_get_info", "fks_get_path",
            "fks_get_fast_layout",
            "fks_get_tables", "fks_get_last_shift", "fks_profile", "fks_profile_read", "fks_debug_timestamps", "fks_launch_count",
-           "fks_sync", "fks_destroy", "fks_last_error"]
+           "fks_sync", "fks_destroy", "fks_last_error", "fks_moments", "fks_bgk_batch", "fks_bgk_step"]
 
 
 class fks_params(C.Structure):
@@ -65,6 +65,9 @@ def load_library(path: str = None):
         "fks_transport_step": ([vp, vp, vp, vp], i),
         "fks_step": ([vp, vp, vp, d, vp], i),
         "fks_step_host": ([vp, vp, vp, d], i),
+        "fks_moments": ([vp, vp, vp, vp, ll, vp], i),
+        "fks_bgk_batch": ([vp, vp, vp, d, ll, vp], i),
+        "fks_bgk_step": ([vp, vp, vp, d, vp, vp, vp], i),
         "fks_get_info": ([vp, C.POINTER(i), C.POINTER(i), dp, dp], i),
         "fks_get_path": ([vp], i),
         "fks_get_fast_layout": ([vp, C.POINTER(i), C.POINTER(i)], i),
@@ -152,6 +155,20 @@ def fks_step(h: int, f_in, f_out, coll_scale: float, stream=None):
 
 def fks_step_host(h: int, f_in_host, f_out_host, coll_scale: float):
     _check(load_library().fks_step_host(h, _ptr(f_in_host), _ptr(f_out_host), coll_scale))
+
+
+def fks_moments(h: int, f, U=None, W=None, n_cells: int | None = None, stream=None):
+    n = f.shape[0] if n_cells is None else n_cells
+    _check(load_library().fks_moments(h, _ptr(f), _ptr(U), _ptr(W), n, _stream(stream)))
+
+
+def fks_bgk_batch(h: int, f, Q, nu: float, n_cells: int | None = None, stream=None):
+    n = f.shape[0] if n_cells is None else n_cells
+    _check(load_library().fks_bgk_batch(h, _ptr(f), _ptr(Q), nu, n, _stream(stream)))
+
+
+def fks_bgk_step(h: int, f_in, f_out, nu_dt: float, U=None, W=None, stream=None):
+    _check(load_library().fks_bgk_step(h, _ptr(f_in), _ptr(f_out), nu_dt, _ptr(U), _ptr(W), _stream(stream)))
 
 
 def fks_get_info(h: int) -> dict:
@@ -250,6 +267,23 @@ class Collision:
 
     def step(self, f_in, f_out, coll_scale: float, stream=None):
         fks_step(self.h, f_in, f_out, coll_scale, stream)
+
+    def moments(self, f, stream=None):
+        """(U, W): conservative (ρ, ρu, E) and primitive (ρ, u, T) moments per cell, [n_cells][5] each."""
+        import torch
+        U = torch.empty((f.shape[0], 5), dtype=torch.float64, device=f.device)
+        W = torch.empty_like(U)
+        fks_moments(self.h, f, U, W, f.shape[0], stream)
+        return U, W
+
+    def bgk_batch(self, f, nu: float, Q=None, stream=None):
+        import torch
+        Q = torch.empty_like(f) if Q is None else Q
+        fks_bgk_batch(self.h, f, Q, nu, f.shape[0], stream)
+        return Q
+
+    def bgk_step(self, f_in, f_out, nu_dt: float, U=None, W=None, stream=None):
+        fks_bgk_step(self.h, f_in, f_out, nu_dt, U, W, stream)
 
     def last_shift(self):
         return fks_get_last_shift(self.h, self.N)

@@ -106,4 +106,9 @@ fks_status fast_prepare(Ctx& c);
 fks_status launch_transport_gather(Ctx& c, const double* fin, double* fout, const Shift& sh, cudaStream_t st,
                                    long long cell0 = 0, long long ncells = -1);
 
+// moments / BGK (macro.cu): mode 0 = moments of fin into U/W, 1 = out = coef (E - fin), 2 = transport by *sh then
+// out = f* + coef (E[f*] - f*).  U, W optional ([n_cells][5]).
+fks_status launch_macro(Ctx& c, int mode, const double* fin, double* out, double* U, double* W, long long n_cells,
+                        double coef, const Shift* sh, cudaStream_t st);
+
 }  // namespace fks

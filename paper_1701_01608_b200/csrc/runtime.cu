@@ -423,6 +423,68 @@ fks_status fks_step_host(fks_ctx* h, const double* f_in_host, double* f_out_host
   return rc ? rc : rs;
 }
 
+// ---- macroscopic moments and the BGK operator (macro.cu) -----------------------------------------------
+static fks_status check_opt_moments(const Ctx& c, double* U, double* W, long long n, const void* f, size_t fbytes) {
+  fks_status rc;
+  const size_t mb = (size_t)n * 5 * sizeof(double);
+  if (U && (rc = check_device_ptr(U, "U"))) return rc;
+  if (W && (rc = check_device_ptr(W, "W"))) return rc;
+  if (U && overlap(U, mb, f, fbytes)) { set_error("U overlaps f"); return FKS_ERR_INVALID; }
+  if (W && overlap(W, mb, f, fbytes)) { set_error("W overlaps f"); return FKS_ERR_INVALID; }
+  if (U && W && overlap(U, mb, W, mb)) { set_error("U overlaps W"); return FKS_ERR_INVALID; }
+  (void)c;
+  return FKS_OK;
+}
+
+fks_status fks_moments(fks_ctx* h, const double* f, double* U, double* W, long long n_cells, void* stream) {
+  if (!h) { set_error("NULL handle"); return FKS_ERR_INVALID; }
+  Ctx& c = *reinterpret_cast<Ctx*>(h);
+  if (n_cells < 0) { set_error("n_cells < 0"); return FKS_ERR_INVALID; }
+  if (n_cells == 0) return FKS_OK;
+  if (!U && !W) { set_error("fks_moments: U and W are both NULL"); return FKS_ERR_INVALID; }
+  fks_status rc;
+  if ((rc = check_device_ptr(f, "f"))) return rc;
+  const size_t bytes = (size_t)n_cells * c.N * c.N * c.N * sizeof(double);
+  if ((rc = check_opt_moments(c, U, W, n_cells, f, bytes))) return rc;
+  if ((rc = sticky_check())) return rc;
+  return launch_macro(c, 0, f, nullptr, U, W, n_cells, 0.0, nullptr, reinterpret_cast<cudaStream_t>(stream));
+}
+
+fks_status fks_bgk_batch(fks_ctx* h, const double* f, double* Q, double nu, long long n_cells, void* stream) {
+  if (!h) { set_error("NULL handle"); return FKS_ERR_INVALID; }
+  Ctx& c = *reinterpret_cast<Ctx*>(h);
+  if (n_cells < 0) { set_error("n_cells < 0"); return FKS_ERR_INVALID; }
+  if (!std::isfinite(nu)) { set_error("nu must be finite"); return FKS_ERR_INVALID; }
+  if (n_cells == 0) return FKS_OK;
+  fks_status rc;
+  if ((rc = check_device_ptr(f, "f")) || (rc = check_device_ptr(Q, "Q"))) return rc;
+  const size_t bytes = (size_t)n_cells * c.N * c.N * c.N * sizeof(double);
+  if (overlap(f, bytes, Q, bytes)) { set_error("Q overlaps f"); return FKS_ERR_INVALID; }
+  if ((rc = sticky_check())) return rc;
+  return launch_macro(c, 1, f, Q, nullptr, nullptr, n_cells, nu, nullptr, reinterpret_cast<cudaStream_t>(stream));
+}
+
+fks_status fks_bgk_step(fks_ctx* h, const double* f_in, double* f_out, double nu_dt, double* U, double* W,
+                        void* stream) {
+  if (!h) { set_error("NULL handle"); return FKS_ERR_INVALID; }
+  Ctx& c = *reinterpret_cast<Ctx*>(h);
+  if (!c.transport_ready) { set_error("fks_transport_setup not called"); return FKS_ERR_STATE; }
+  if (!std::isfinite(nu_dt)) { set_error("nu_dt must be finite"); return FKS_ERR_INVALID; }
+  fks_status rc;
+  if ((rc = check_device_ptr(f_in, "f_in")) || (rc = check_device_ptr(f_out, "f_out"))) return rc;
+  const long long n = (long long)c.nx * c.ny * c.nz;
+  const size_t bytes = (size_t)n * c.N * c.N * c.N * sizeof(double);
+  if (overlap(f_in, bytes, f_out, bytes)) { set_error("f_out overlaps f_in"); return FKS_ERR_INVALID; }
+  if ((rc = check_opt_moments(c, U, W, n, f_in, bytes))) return rc;
+  if ((U && overlap(U, (size_t)n * 40, f_out, bytes)) || (W && overlap(W, (size_t)n * 40, f_out, bytes))) {
+    set_error("U/W overlap f_out");
+    return FKS_ERR_INVALID;
+  }
+  if ((rc = sticky_check())) return rc;
+  Shift sh = advance_generic_cell(c);
+  return launch_macro(c, 2, f_in, f_out, U, W, n, nu_dt, &sh, reinterpret_cast<cudaStream_t>(stream));
+}
+
 fks_status fks_get_info(const fks_ctx* h, int* P, int* T, double* R, double* lambda) {
   if (!h) { set_error("NULL handle"); return FKS_ERR_INVALID; }
   const Ctx& c = *reinterpret_cast<const Ctx*>(h);
