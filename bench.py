@@ -301,6 +301,10 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--decomposed", action="store_true",
+                    help="N ranks run ONE periodic box of N x 32 x-planes, slab-decomposed in x (fks_step_slab: the "
+                         "transport gathers across slab boundaries from the neighbours' memory over NVLink, one "
+                         "barrier per step) instead of N independent boxes")
     ap.add_argument("--workload", default="boltzmann", choices=["boltzmann", "bgk"],
                     help="bgk: the BGK-operator FKS step (SURVEY §8(f) NEXT-3; HBM-bound) on the same config")
     args = ap.parse_args()
@@ -366,8 +370,21 @@ def main():
             dist.barrier()
 
     bufs = [fa, fb]
+    stepper = None
+    if args.decomposed:  # one global box, x-slab per rank (rank r's own c3 box is its slab)
+        dom = D.SlabDomain(cfg.shape[0] * ws, cfg.shape[1], cfg.shape[2], rank, ws)
+        stepper = D.SlabStepper(col, dom, fa, fb, cfg.cfl_num, cfg.cfl_den, barrier=D.stream_barrier(dev))
+        workload["workload"] += f"; decomposed: one {cfg.shape[0] * ws}x{cfg.shape[1]}x{cfg.shape[2]} box, x-slabs"
+        workload["parallelism"] = f"x-slabs over {ws} ranks, peer-memory transport gather"
+
+    def one_step(i):
+        if stepper is not None:
+            stepper.step(s)
+        else:
+            col.step(bufs[i % 2], bufs[(i + 1) % 2], s)
+
     for i in range(args.warmup):
-        col.step(bufs[i % 2], bufs[(i + 1) % 2], s)
+        one_step(i)
     torch.cuda.synchronize()
     barrier()
     B.fks_profile(col.h, True)
@@ -379,7 +396,7 @@ def main():
         barrier()
         e0.record(stream)
         for i in range(args.steps):
-            col.step(bufs[(args.warmup + i) % 2], bufs[(args.warmup + i + 1) % 2], s)
+            one_step(args.warmup + i)
         e1.record(stream)
         torch.cuda.synchronize()
         barrier()
@@ -412,7 +429,7 @@ def main():
 
     # end to end through the host-buffer C-ABI call (pinned host memory, copies inside the timed region)
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not args.decomposed:
         hin = torch.empty(fa.shape, dtype=torch.float64, pin_memory=True)
         hout = torch.empty_like(hin, pin_memory=True)
         hin.copy_(fa)

@@ -102,6 +102,28 @@ fks_status fks_step(fks_ctx* h, const double* f_in, double* f_out, double coll_s
 /* Host-buffer variant of fks_step (synchronous), for the end-to-end measurement. */
 fks_status fks_step_host(fks_ctx* h, const double* f_in_host, double* f_out_host, double coll_scale);
 
+/* Slab decomposition in x for one process per GPU (the paper's MPI FKS).
+ * This handle owns the global x-planes [x0, x0 + nx_local) of a periodic nx_global x ny x nz grid; every rank
+ * runs the same generic-cell bookkeeping (identical shifts).  Afterwards only the _slab calls below (and the
+ * collision calls) are valid on the handle; fks_transport_setup returns it to a single domain. */
+fks_status fks_transport_setup_slab(fks_ctx* h, int nx_global, int ny, int nz, int x0, int nx_local,
+                                    long long cfl_num, long long cfl_den);
+
+/* Halo width H = an upper bound of max |delta_x| over all steps (ceil(cfl) + 1). */
+fks_status fks_slab_halo(const fks_ctx* h, int* halo);
+
+/* One transport step of the local cells, gathering across the slab boundary directly from the owner's memory:
+ * `planes` is a HOST array of nx_local + 2H DEVICE pointers; planes[i] is global x-plane (x0 - H + i) mod
+ * nx_global, laid out [ny][nz][N][N][N] fp64 (this rank's own planes, or a neighbour's mapped through CUDA IPC /
+ * peer access: the kernel loads them over NVLink, no separate halo exchange).  f_out: local
+ * [nx_local*ny*nz][N^3]; must not overlap any plane.  The caller orders the steps across ranks: a rank may
+ * overwrite a buffer only after every rank that reads it finished the previous step (e.g. one barrier per step).
+ * Bit-identical to fks_transport_step on the whole grid. */
+fks_status fks_transport_step_slab(fks_ctx* h, const double* const* planes, double* f_out, void* stream);
+
+/* Slab variant of fks_step: the gather above, then collision + Euler on the local cells in place in f_out. */
+fks_status fks_step_slab(fks_ctx* h, const double* const* planes, double* f_out, double coll_scale, void* stream);
+
 /* Macroscopic moments per cell ("ToConservative" / "ToPrimitive"):
  *   U[c] = sum_k phi(v_k) f[c][k] dv^3 = (rho, rho u_x, rho u_y, rho u_z, E),  phi = (1, v, |v|^2/2), dv = 2L/N;
  *   W[c] = (rho, u_x, u_y, u_z, T) with (3/2) rho T = E - rho |u|^2 / 2.

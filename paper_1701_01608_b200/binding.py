@@ -24,7 +24,8 @@ EXPORTS = ["fks_collision_init", "fks_collision_init_ex", "fks_collision_batch",
            "fks_transport_setup", "fks_transport_step", "fks_step", "fks_step_host", "fks_get_info", "fks_get_path",
            "fks_get_fast_layout",
            "fks_get_tables", "fks_get_last_shift", "fks_profile", "fks_profile_read", "fks_debug_timestamps", "fks_launch_count",
-           "fks_sync", "fks_destroy", "fks_last_error", "fks_moments", "fks_bgk_batch", "fks_bgk_step"]
+           "fks_sync", "fks_destroy", "fks_last_error", "fks_moments", "fks_bgk_batch", "fks_bgk_step",
+           "fks_transport_setup_slab", "fks_slab_halo", "fks_transport_step_slab", "fks_step_slab"]
 
 
 class fks_params(C.Structure):
@@ -66,6 +67,10 @@ def load_library(path: str = None):
         "fks_step": ([vp, vp, vp, d, vp], i),
         "fks_step_host": ([vp, vp, vp, d], i),
         "fks_moments": ([vp, vp, vp, vp, ll, vp], i),
+        "fks_transport_setup_slab": ([vp, i, i, i, i, i, ll, ll], i),
+        "fks_slab_halo": ([vp, C.POINTER(i)], i),
+        "fks_transport_step_slab": ([vp, vp, vp, vp], i),
+        "fks_step_slab": ([vp, vp, vp, d, vp], i),
         "fks_bgk_batch": ([vp, vp, vp, d, ll, vp], i),
         "fks_bgk_step": ([vp, vp, vp, d, vp, vp, vp], i),
         "fks_get_info": ([vp, C.POINTER(i), C.POINTER(i), dp, dp], i),
@@ -155,6 +160,33 @@ def fks_step(h: int, f_in, f_out, coll_scale: float, stream=None):
 
 def fks_step_host(h: int, f_in_host, f_out_host, coll_scale: float):
     _check(load_library().fks_step_host(h, _ptr(f_in_host), _ptr(f_out_host), coll_scale))
+
+
+def fks_transport_setup_slab(h: int, nx_global: int, ny: int, nz: int, x0: int, nx_local: int, cfl_num: int,
+                             cfl_den: int):
+    _check(load_library().fks_transport_setup_slab(h, nx_global, ny, nz, x0, nx_local, cfl_num, cfl_den))
+
+
+def fks_slab_halo(h: int) -> int:
+    H = C.c_int()
+    _check(load_library().fks_slab_halo(h, C.byref(H)))
+    return H.value
+
+
+def _plane_array(planes):
+    """HOST array of device pointers (ints or tensors) for the _slab calls."""
+    arr = (C.c_void_p * len(planes))()
+    for i, p in enumerate(planes):
+        arr[i] = _ptr(p)
+    return arr
+
+
+def fks_transport_step_slab(h: int, planes, f_out, stream=None):
+    _check(load_library().fks_transport_step_slab(h, _plane_array(planes), _ptr(f_out), _stream(stream)))
+
+
+def fks_step_slab(h: int, planes, f_out, coll_scale: float, stream=None):
+    _check(load_library().fks_step_slab(h, _plane_array(planes), _ptr(f_out), coll_scale, _stream(stream)))
 
 
 def fks_moments(h: int, f, U=None, W=None, n_cells: int | None = None, stream=None):

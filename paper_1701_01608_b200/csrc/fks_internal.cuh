@@ -65,6 +65,8 @@ struct Ctx {
   cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;  // host-buffer step pipeline
   // transport state (generic cell)
   bool transport_ready = false;
+  bool slab = false;                    // slab decomposition in x (fks_transport_setup_slab): this handle owns
+  int nx_glob = 0, x0 = 0, halo = 0;    // global x-planes [x0, x0 + nx) of nx_glob; halo = max |delta_x|
   int nx = 0, ny = 0, nz = 0;
   long long cfl_num = 0, cfl_den = 1;
   std::vector<long long> offsets;       // [3][N] in units of 1/(N*cfl_den) cell
@@ -105,6 +107,14 @@ fks_status fast_prepare(Ctx& c);
 // transport gather (transport.cu)
 fks_status launch_transport_gather(Ctx& c, const double* fin, double* fout, const Shift& sh, cudaStream_t st,
                                    long long cell0 = 0, long long ncells = -1);
+
+// slab-decomposed transport (transport.cu): x-plane pointer table, plane i = global plane (x0 - halo + i) mod
+// nx_glob, each [ny][nz][N^3] (local or peer memory)
+constexpr int kMaxPlanes = 1024;
+struct PlaneTable {
+  const double* p[kMaxPlanes];
+};
+fks_status launch_transport_gather_slab(Ctx& c, const PlaneTable& tab, double* fout, const Shift& sh, cudaStream_t st);
 
 // moments / BGK (macro.cu): mode 0 = moments of fin into U/W, 1 = out = coef (E - fin), 2 = transport by *sh then
 // out = f* + coef (E[f*] - f*).  U, W optional ([n_cells][5]).

@@ -281,13 +281,92 @@ fks_status fks_transport_setup(fks_ctx* h, int nx, int ny, int nz, long long cfl
   c.cfl_num = cfl_num; c.cfl_den = cfl_den;
   std::fill(c.offsets.begin(), c.offsets.end(), 0);
   c.transport_ready = true;
+  c.slab = false;
+  c.nx_glob = nx; c.x0 = 0; c.halo = 0;
   return FKS_OK;
+}
+
+// max |delta| of any step: |displacement| <= N cfl_num units = cfl cells, offsets in [-1/2, 1/2)
+static int halo_bound(long long cfl_num, long long cfl_den) { return (int)((cfl_num + cfl_den - 1) / cfl_den) + 1; }
+
+fks_status fks_transport_setup_slab(fks_ctx* h, int nx_global, int ny, int nz, int x0, int nx_local,
+                                    long long cfl_num, long long cfl_den) {
+  if (!h) { set_error("NULL handle"); return FKS_ERR_INVALID; }
+  Ctx& c = *reinterpret_cast<Ctx*>(h);
+  if (nx_local < 1 || x0 < 0 || x0 + (long long)nx_local > nx_global) {
+    set_error("slab: need 0 <= x0 and 1 <= nx_local, x0 + nx_local <= nx_global");
+    return FKS_ERR_INVALID;
+  }
+  fks_status rc = fks_transport_setup(h, nx_local, ny, nz, cfl_num, cfl_den);
+  if (rc) return rc;
+  const int H = halo_bound(cfl_num, cfl_den);
+  if (nx_local + 2LL * H > kMaxPlanes) { set_error("slab: nx_local + 2*halo exceeds 1024 planes"); return FKS_ERR_UNSUPPORTED; }
+  c.slab = true;
+  c.nx_glob = nx_global; c.x0 = x0; c.halo = H;
+  return FKS_OK;
+}
+
+fks_status fks_slab_halo(const fks_ctx* h, int* halo) {
+  if (!h || !halo) { set_error("NULL argument"); return FKS_ERR_INVALID; }
+  const Ctx& c = *reinterpret_cast<const Ctx*>(h);
+  if (!c.transport_ready || !c.slab) { set_error("fks_transport_setup_slab not called"); return FKS_ERR_STATE; }
+  *halo = c.halo;
+  return FKS_OK;
+}
+
+static fks_status slab_table(Ctx& c, const double* const* planes, double* f_out, PlaneTable& tab) {
+  if (!c.transport_ready || !c.slab) { set_error("fks_transport_setup_slab not called"); return FKS_ERR_STATE; }
+  if (!planes) { set_error("planes is NULL"); return FKS_ERR_INVALID; }
+  fks_status rc;
+  if ((rc = check_device_ptr(f_out, "f_out"))) return rc;
+  const int np = c.nx + 2 * c.halo;
+  const size_t plane_bytes = (size_t)c.ny * c.nz * c.N * c.N * c.N * sizeof(double);
+  const size_t out_bytes = plane_bytes * c.nx;
+  for (int i = 0; i < np; i++) {
+    if (!planes[i]) { set_error("planes[i] is NULL"); return FKS_ERR_INVALID; }
+    if (overlap(planes[i], plane_bytes, f_out, out_bytes)) { set_error("a source plane overlaps f_out"); return FKS_ERR_INVALID; }
+    tab.p[i] = planes[i];
+  }
+  return FKS_OK;
+}
+
+fks_status fks_transport_step_slab(fks_ctx* h, const double* const* planes, double* f_out, void* stream) {
+  if (!h) { set_error("NULL handle"); return FKS_ERR_INVALID; }
+  Ctx& c = *reinterpret_cast<Ctx*>(h);
+  static thread_local PlaneTable tab;
+  fks_status rc;
+  if ((rc = slab_table(c, planes, f_out, tab))) return rc;
+  if ((rc = sticky_check())) return rc;
+  Shift sh = advance_generic_cell(c);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  c.prof.begin(0, st);
+  rc = launch_transport_gather_slab(c, tab, f_out, sh, st);
+  c.prof.end(0, st);
+  return rc;
+}
+
+fks_status fks_step_slab(fks_ctx* h, const double* const* planes, double* f_out, double coll_scale, void* stream) {
+  if (!h) { set_error("NULL handle"); return FKS_ERR_INVALID; }
+  Ctx& c = *reinterpret_cast<Ctx*>(h);
+  if (!std::isfinite(coll_scale)) { set_error("coll_scale must be finite"); return FKS_ERR_INVALID; }
+  static thread_local PlaneTable tab;
+  fks_status rc;
+  if ((rc = slab_table(c, planes, f_out, tab))) return rc;
+  if ((rc = sticky_check())) return rc;
+  Shift sh = advance_generic_cell(c);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  c.prof.begin(0, st);
+  rc = launch_transport_gather_slab(c, tab, f_out, sh, st);
+  c.prof.end(0, st);
+  if (rc) return rc;
+  return run_collision(c, f_out, f_out, (long long)c.nx * c.ny * c.nz, true, coll_scale, st);
 }
 
 fks_status fks_transport_step(fks_ctx* h, const double* f_in, double* f_out, void* stream) {
   if (!h) { set_error("NULL handle"); return FKS_ERR_INVALID; }
   Ctx& c = *reinterpret_cast<Ctx*>(h);
   if (!c.transport_ready) { set_error("fks_transport_setup not called"); return FKS_ERR_STATE; }
+  if (c.slab) { set_error("handle is set up for a slab: use the _slab calls"); return FKS_ERR_STATE; }
   fks_status rc;
   if ((rc = check_device_ptr(f_in, "f_in")) || (rc = check_device_ptr(f_out, "f_out"))) return rc;
   long long n = (long long)c.nx * c.ny * c.nz;
@@ -306,6 +385,7 @@ fks_status fks_step(fks_ctx* h, const double* f_in, double* f_out, double coll_s
   if (!h) { set_error("NULL handle"); return FKS_ERR_INVALID; }
   Ctx& c = *reinterpret_cast<Ctx*>(h);
   if (!c.transport_ready) { set_error("fks_transport_setup not called"); return FKS_ERR_STATE; }
+  if (c.slab) { set_error("handle is set up for a slab: use the _slab calls"); return FKS_ERR_STATE; }
   if (!std::isfinite(coll_scale)) { set_error("coll_scale must be finite"); return FKS_ERR_INVALID; }
   fks_status rc;
   if ((rc = check_device_ptr(f_in, "f_in")) || (rc = check_device_ptr(f_out, "f_out"))) return rc;
@@ -362,6 +442,7 @@ fks_status fks_step_host(fks_ctx* h, const double* f_in_host, double* f_out_host
   if (!h) { set_error("NULL handle"); return FKS_ERR_INVALID; }
   Ctx& c = *reinterpret_cast<Ctx*>(h);
   if (!c.transport_ready) { set_error("fks_transport_setup not called"); return FKS_ERR_STATE; }
+  if (c.slab) { set_error("handle is set up for a slab: use the _slab calls"); return FKS_ERR_STATE; }
   if (!f_in_host || !f_out_host) { set_error("bad host buffers"); return FKS_ERR_INVALID; }
   if (!std::isfinite(coll_scale)) { set_error("coll_scale must be finite"); return FKS_ERR_INVALID; }
   const long long n = (long long)c.nx * c.ny * c.nz;
@@ -469,6 +550,7 @@ fks_status fks_bgk_step(fks_ctx* h, const double* f_in, double* f_out, double nu
   if (!h) { set_error("NULL handle"); return FKS_ERR_INVALID; }
   Ctx& c = *reinterpret_cast<Ctx*>(h);
   if (!c.transport_ready) { set_error("fks_transport_setup not called"); return FKS_ERR_STATE; }
+  if (c.slab) { set_error("handle is set up for a slab: use the _slab calls"); return FKS_ERR_STATE; }
   if (!std::isfinite(nu_dt)) { set_error("nu_dt must be finite"); return FKS_ERR_INVALID; }
   fks_status rc;
   if ((rc = check_device_ptr(f_in, "f_in")) || (rc = check_device_ptr(f_out, "f_out"))) return rc;
