@@ -353,10 +353,13 @@ def beta_matrix(tables: Tables) -> np.ndarray:
     return tables.a.reshape(-1, n).T @ tables.b.reshape(-1, n)
 
 
-def collision_direct(f: np.ndarray, tables: Tables, project_mass: bool = False) -> np.ndarray:
+def collision_direct(f: np.ndarray, tables: Tables, project_mass: bool = False, P: int | None = None) -> np.ndarray:
     """Direct O(N^6) Galerkin double sum Q̂_k = Σ_{l+m=k} β̂(l,m) f̂_l f̂_m (Eq. CF1).
 
-    Guarded to N ≤ 24 (the β̂ matrix has (N−1)^6 entries)."""
+    With P given (N ≤ P < 3N/2 − 2): the aliased collocation operator of a P-point product grid (SURVEY §8(f)
+    NEXT-4 (ii); P = N is the classical collocation spectral method), Q̂_k = Σ_{l+m ≡ k (mod P)} β̂(l,m) f̂_l f̂_m
+    per axis — the pair (l, m) contributes to the k ∈ K' congruent to l + m, if any.  P ≥ 3N/2 − 2 gives back
+    the exact sum.  Guarded to N ≤ 24 (the β̂ matrix has (N−1)^6 entries)."""
     N = f.shape[-1]
     if N > 24:
         raise ValueError("direct sum guarded to N <= 24")
@@ -365,8 +368,27 @@ def collision_direct(f: np.ndarray, tables: Tables, project_mass: bool = False) 
     fh = forward_modes(f)
     beta = beta_matrix(tables).reshape((n1,) * 6)
     Qh = np.zeros((n1, n1, n1), dtype=np.complex128)
-    # index i ↔ mode K[i] = i - c;  k = l + m ∈ K' ⟺ 0 ≤ il + im − c < n1
     c = N // 2 - 1
+    if P is not None:
+        # aliased: every (l, m) pair, target k = ((l + m + c) mod P) − c when that lies in K'
+        if P < N:
+            raise ValueError("P >= N")
+        s = K[:, None] + K[None, :]                       # l + m per axis
+        kk = np.mod(s + c, P) - c
+        valid = np.abs(kk) <= c
+        tgt = kk + c                                      # index of k
+        for ix in range(n1):
+            for iy in range(n1):
+                for iz in range(n1):
+                    vx, vy, vz = valid[ix], valid[iy], valid[iz]
+                    mx, my, mz = np.nonzero(vx)[0], np.nonzero(vy)[0], np.nonzero(vz)[0]
+                    b = beta[ix, iy, iz][np.ix_(mx, my, mz)]
+                    contrib = fh[ix, iy, iz] * b * fh[np.ix_(mx, my, mz)]
+                    np.add.at(Qh, np.ix_(tgt[ix, mx], tgt[iy, my], tgt[iz, mz]), contrib)
+        if project_mass:
+            Qh[c, c, c] = 0.0
+        return inverse_modes(Qh, N).real
+    # index i ↔ mode K[i] = i - c;  k = l + m ∈ K' ⟺ 0 ≤ il + im − c < n1
     for ix in range(n1):
         for iy in range(n1):
             for iz in range(n1):
