@@ -35,7 +35,7 @@ typedef struct fks_ctx fks_ctx;
 typedef enum {
   FKS_OK = 0,
   FKS_ERR_INVALID = 1,      /* bad argument, overlapping buffers, host pointer where a device pointer is needed */
-  FKS_ERR_UNSUPPORTED = 2,  /* N odd, N < 4, N > 64, P < 3N/2-2, unknown kernel/rule, requested path unavailable */
+  FKS_ERR_UNSUPPORTED = 2,  /* N odd, N < 4, N > 64, P < N or P > 4N, unknown kernel/rule, requested path unavailable */
   FKS_ERR_NOMEM = 3,        /* device allocation failed */
   FKS_ERR_CUDA = 4,         /* launch failure or asynchronous CUDA error (sticky errors stay sticky) */
   FKS_ERR_STATE = 5         /* e.g. fks_transport_step / fks_step before fks_transport_setup */
@@ -65,7 +65,9 @@ typedef struct {
   int kernel;                   /* fks_kernel                                                              */
   int n_theta, n_phi;           /* 0,0 = derive from M_angles (A12)                                        */
   int quad_rule;                /* fks_quad                                                                */
-  int pad;                      /* 0 = P = 3N/2 (default, A10); else explicit P >= 3N/2 - 2                */
+  int pad;                      /* 0 = P = 3N/2 (default, A10); else explicit P in [N, 4N]: P >= 3N/2-2 is
+                                   the exact Galerkin operator, P < 3N/2-2 the aliased collocation operator
+                                   (pairs with l+m = k mod P; P = N: classical collocation; generic path)   */
   double cutoff_ratio;          /* Carleman cutoff R_c = ratio*R; 0 or 1 = paper-literal (A7), max 1.7072  */
   int project_mass;             /* 1 = set Q^_0 := 0 exactly (A24); default 0                              */
   long long max_cells_in_flight;/* workspace limit in cells per chunk; 0 = auto                            */

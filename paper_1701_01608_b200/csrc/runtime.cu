@@ -199,7 +199,9 @@ fks_status fks_collision_init_ex(fks_ctx** out, const fks_params* pp) {
   }
   if (p.path < FKS_PATH_AUTO || p.path > FKS_PATH_FAST) { set_error("unknown path"); return FKS_ERR_UNSUPPORTED; }
   int P = p.pad > 0 ? p.pad : 3 * p.N / 2;
-  if (P < 3 * p.N / 2 - 2 || P > 4 * p.N) { set_error("pad must be >= 3N/2 - 2 (A10)"); return FKS_ERR_UNSUPPORTED; }
+  // P >= 3N/2 - 2: the exact Galerkin operator (A10); N <= P < 3N/2 - 2: the aliased collocation operator
+  // (l + m = k mod P; P = N is the classical collocation method)
+  if (P < p.N || P > 4 * p.N) { set_error("pad must be in [N, 4N] (A10; P < 3N/2-2 is the aliased variant)"); return FKS_ERR_UNSUPPORTED; }
   int nt = p.n_theta, nf = p.n_phi;
   if (nt <= 0 || nf <= 0) {
     nt = 1 << (int)std::ceil(std::log2((double)p.M_angles) / 2.0 - 1e-12);

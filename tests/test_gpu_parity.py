@@ -88,6 +88,31 @@ def test_collision_pad_and_projection(cuda_device, pad):
     assert np.abs(Q.reshape(3, -1).sum(1)).max() <= 1e-13 * np.abs(Q).max() * Q[0].size
 
 
+@pytest.mark.parametrize("N", [6, 8, 12, 16])
+def test_collision_aliased_variant_vs_direct_sum(cuda_device, N):
+    """pad P < 3N/2 - 2 is the aliased collocation operator (P = N: classical collocation),
+    compared with the oracle's brute-force sum over l + m = k mod P (pinned, P24)."""
+    tb = oracle_tables(N, L_BOX, 16, 4, 0)
+    f = inputs.random_field(3, N, seed=40 + N, signed=False).to(cuda_device)
+    for P in sorted({N, N + 2, 3 * N // 2 - 3}):
+        if P < N:
+            continue
+        col = B.Collision(N, L_BOX, 16, 4, 0, pad=P)
+        assert col.info["P"] == P and col.info["path"] == B.FKS_PATH_GENERIC
+        Q = col.collision_batch(f).cpu().numpy()
+        ref = np.stack([o.collision_direct(x, tb, P=P) for x in f.cpu().numpy()])
+        assert rel_err_per_cell(Q, ref).max() <= TOL_Q, P
+
+
+def test_collision_aliased_N32_P32(cuda_device):
+    cfg = CONFIGS["c2"]
+    f = inputs.make_f(cfg, device=cuda_device, cells=[0, 300])
+    col = B.Collision(cfg.N, cfg.L, cfg.M, cfg.M_r, cfg.kernel, pad=32)
+    Q = col.collision_batch(f).cpu().numpy()
+    ref = oracle_Q(f.cpu().numpy(), cfg_tables("c2"), P=32)
+    assert rel_err_per_cell(Q, ref).max() <= TOL_Q
+
+
 def test_collision_bkw_report(cuda_device):
     """c1 (BKW, N = 24): Q vs the analytic ∂f/∂t.  Resolution-limited (~0.2-0.5, P14): reported,
     gated only loosely; the 1e-6 BKW pin is the oracle's N = 64 test."""
