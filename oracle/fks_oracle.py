@@ -39,6 +39,8 @@ LAMBDA = 2.0 / (3.0 + math.sqrt(2.0))
 
 KERNEL_HARD_SPHERES = 0  # B~ ≡ 1 (A4)
 KERNEL_MAXWELL = 1       # B~ = (1/π)(|x|²+|y|²)^{-1/2} (Eq. Btilde_pl with α=0; A5)
+KERNEL_VHS = 2           # B = C_α|u|^α, 0 ≤ α ≤ 1: B~ = 4C_α(|x|²+|y|²)^{-(1-α)/2} (A30)
+VHS_C_DEFAULT = 1.0 / (4.0 * math.pi)  # C_α default: α = 0 is the Maxwell-molecule normalisation (A5)
 
 QUAD_GL_UNIFORM = 0      # Gauss-Legendre in cos θ × uniform φ on the half sphere (A11, A12)
 QUAD_PAPER_RECT = 1      # (θ_p, φ_q) = (pπ/A1, qπ/A2), weight π²/(A1A2)·sin θ_p (A2)
@@ -170,9 +172,13 @@ def _xi_grid(N: int, L: float):
 
 
 def iter_terms(N: int, L: float, M: int = 16, M_r: int = 16, kernel: int = KERNEL_HARD_SPHERES,
-               n_theta: int = 0, n_phi: int = 0, rule: int = QUAD_GL_UNIFORM, cutoff_ratio: float = 1.0):
+               n_theta: int = 0, n_phi: int = 0, rule: int = QUAD_GL_UNIFORM, cutoff_ratio: float = 1.0,
+               alpha: float = 0.5, C_alpha: float = VHS_C_DEFAULT):
     """Yield (a_t, b_t) for t = 1..T in order — step by step as in DESIGN.md §2.2
-    (P:1612-1632 with readings A1-A7, A11, A12).  HS: t = 1 + d.  MM: t = 1 + d·M_r + i."""
+    (P:1612-1632 with readings A1-A7, A11, A12).  HS: t = 1 + d.  MM and VHS: t = 1 + d·M_r + i.
+
+    VHS (A30): the same radial split as MM with B~(ρ_i, ρ_j) = 4C_α(ρ_i²+ρ_j²)^{(α−1)/2}, i.e.
+    b_t = 2π Σ_j W_jρ_j B~(ρ_i, ρ_j) J₀(ρ_j τ)  (MM: 4C_0 = 1/π gives the factor 2 above)."""
     R = support_radius(L)
     Rc = R * (cutoff_ratio if cutoff_ratio > 0 else 1.0)  # Carleman cutoff x, y ∈ B_Rc (A7)
     if n_theta <= 0 or n_phi <= 0:
@@ -195,18 +201,30 @@ def iter_terms(N: int, L: float, M: int = 16, M_r: int = 16, kernel: int = KERNE
             for i in range(M_r):
                 yield (w[d] * 2.0 * Wr[i] * rho[i] * np.cos(rho[i] * s),
                        2.0 * np.tensordot(Wr * rho * Bt[i], J0, axes=(0, 0)))
+    elif kernel == KERNEL_VHS:
+        if not 0.0 <= alpha <= 1.0:
+            raise ValueError("VHS needs 0 <= alpha <= 1")
+        rho, Wr = gauss_legendre(M_r, 0.0, Rc)
+        Bt = 4.0 * C_alpha * (rho[:, None] ** 2 + rho[None, :] ** 2) ** ((alpha - 1.0) / 2.0)  # B~(ρ_i, ρ_j)
+        for d in range(e.shape[0]):
+            s = xi @ e[d]
+            tau = np.sqrt(np.maximum(xi2 - s * s, 0.0))
+            J0 = special.j0(rho[:, None, None, None] * tau[None])
+            for i in range(M_r):
+                yield (w[d] * 2.0 * Wr[i] * rho[i] * np.cos(rho[i] * s),
+                       2.0 * math.pi * np.tensordot(Wr * rho * Bt[i], J0, axes=(0, 0)))
     else:
         raise ValueError("unknown kernel")
 
 
 def build_tables(N: int, L: float, M: int = 16, M_r: int = 16, kernel: int = KERNEL_HARD_SPHERES,
                  n_theta: int = 0, n_phi: int = 0, rule: int = QUAD_GL_UNIFORM,
-                 cutoff_ratio: float = 1.0) -> Tables:
+                 cutoff_ratio: float = 1.0, alpha: float = 0.5, C_alpha: float = VHS_C_DEFAULT) -> Tables:
     """Materialise all terms, then the loss term t = 0: a_0 = 1, b_0 = −Σ_{t≥1} a_t b_t."""
     if n_theta <= 0 or n_phi <= 0:
         n_theta, n_phi = split_angles(M)
     e, w = directions(n_theta, n_phi, rule)
-    terms = list(iter_terms(N, L, M, M_r, kernel, n_theta, n_phi, rule, cutoff_ratio))
+    terms = list(iter_terms(N, L, M, M_r, kernel, n_theta, n_phi, rule, cutoff_ratio, alpha, C_alpha))
     a = np.stack([t[0] for t in terms])
     b = np.stack([t[1] for t in terms])
     a0 = np.ones((1,) + a.shape[1:])
