@@ -43,7 +43,9 @@ typedef enum {
 
 typedef enum {
   FKS_KERNEL_HARD_SPHERES = 0,  /* B~ = 1          (B = |u|/4, A4)                 */
-  FKS_KERNEL_MAXWELL = 1        /* B~ = (1/pi)(|x|^2+|y|^2)^(-1/2)  (B = 1/(4 pi); Eq. Btilde_pl, A5) */
+  FKS_KERNEL_MAXWELL = 1,       /* B~ = (1/pi)(|x|^2+|y|^2)^(-1/2)  (B = 1/(4 pi); Eq. Btilde_pl, A5) */
+  FKS_KERNEL_VHS = 2            /* variable hard spheres B = C_a |u|^a, 0 <= a <= 1:
+                                   B~ = 4 C_a (|x|^2+|y|^2)^(-(1-a)/2), radial split as Maxwell molecules (A30) */
 } fks_kernel;
 
 typedef enum {
@@ -61,7 +63,7 @@ typedef struct {
   int N;                        /* velocity points per axis, even, 4..64                                   */
   double L;                     /* half-width of the periodic velocity box [-L, L)^3; support R = lambda*L  */
   int M_angles;                 /* number of half-sphere directions (A12: n_theta = 2^ceil(log2(M)/2))      */
-  int M_radial;                 /* Maxwell molecules: radial GL nodes on [0, R_c] (>= 1); HS: unused       */
+  int M_radial;                 /* Maxwell molecules / VHS: radial GL nodes on [0, R_c] (>= 1); HS: unused */
   int kernel;                   /* fks_kernel                                                              */
   int n_theta, n_phi;           /* 0,0 = derive from M_angles (A12)                                        */
   int quad_rule;                /* fks_quad                                                                */
@@ -72,6 +74,8 @@ typedef struct {
   int project_mass;             /* 1 = set Q^_0 := 0 exactly (A24); default 0                              */
   long long max_cells_in_flight;/* workspace limit in cells per chunk; 0 = auto                            */
   int path;                     /* fks_path                                                                */
+  double vhs_alpha;             /* FKS_KERNEL_VHS: exponent a in [0, 1]                                    */
+  double vhs_C;                 /* FKS_KERNEL_VHS: C_a > 0; 0 = 1/(4 pi) (a = 0 is then Maxwell molecules) */
 } fks_params;
 
 /* Precompute the separated-kernel weight tables a_t, b_t (t = 0..T) on the device (A1-A7).

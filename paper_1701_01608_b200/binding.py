@@ -32,7 +32,8 @@ class fks_params(C.Structure):
     _fields_ = [("N", C.c_int), ("L", C.c_double), ("M_angles", C.c_int), ("M_radial", C.c_int),
                 ("kernel", C.c_int), ("n_theta", C.c_int), ("n_phi", C.c_int), ("quad_rule", C.c_int),
                 ("pad", C.c_int), ("cutoff_ratio", C.c_double), ("project_mass", C.c_int),
-                ("max_cells_in_flight", C.c_longlong), ("path", C.c_int)]
+                ("max_cells_in_flight", C.c_longlong), ("path", C.c_int), ("vhs_alpha", C.c_double),
+                ("vhs_C", C.c_double)]
 
 
 class FksError(RuntimeError):

@@ -191,8 +191,15 @@ fks_status fks_collision_init_ex(fks_ctx** out, const fks_params* pp) {
   if (p.N % 2 != 0 || p.N < 4 || p.N > kMaxN) { set_error("N must be even and in [4, 64]"); return FKS_ERR_UNSUPPORTED; }
   if (!(p.L > 0.0) || !std::isfinite(p.L)) { set_error("L must be > 0"); return FKS_ERR_INVALID; }
   if (p.M_angles < 1) { set_error("M_angles must be >= 1"); return FKS_ERR_INVALID; }
-  if (p.kernel != FKS_KERNEL_HARD_SPHERES && p.kernel != FKS_KERNEL_MAXWELL) { set_error("unknown kernel"); return FKS_ERR_UNSUPPORTED; }
-  if (p.kernel == FKS_KERNEL_MAXWELL && p.M_radial < 1) { set_error("M_radial must be >= 1 for Maxwell molecules"); return FKS_ERR_INVALID; }
+  if (p.kernel != FKS_KERNEL_HARD_SPHERES && p.kernel != FKS_KERNEL_MAXWELL && p.kernel != FKS_KERNEL_VHS) {
+    set_error("unknown kernel");
+    return FKS_ERR_UNSUPPORTED;
+  }
+  if (p.kernel != FKS_KERNEL_HARD_SPHERES && p.M_radial < 1) { set_error("M_radial must be >= 1 for Maxwell molecules / VHS"); return FKS_ERR_INVALID; }
+  if (p.kernel == FKS_KERNEL_VHS && !(p.vhs_alpha >= 0.0 && p.vhs_alpha <= 1.0 && p.vhs_C >= 0.0 && std::isfinite(p.vhs_C))) {
+    set_error("VHS needs 0 <= vhs_alpha <= 1 and vhs_C >= 0 (0 = 1/(4 pi))");
+    return FKS_ERR_INVALID;
+  }
   if (p.quad_rule != FKS_QUAD_GL_UNIFORM && p.quad_rule != FKS_QUAD_PAPER_RECT) { set_error("unknown quadrature rule"); return FKS_ERR_UNSUPPORTED; }
   if (p.cutoff_ratio < 0.0 || p.cutoff_ratio > (1.0 + std::sqrt(2.0)) / std::sqrt(2.0) + 1e-12) {
     set_error("cutoff_ratio must be in [1, (1+sqrt2)/sqrt2] (A7)"); return FKS_ERR_INVALID;

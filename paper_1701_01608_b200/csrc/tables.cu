@@ -127,7 +127,7 @@ __global__ void twiddle_kernel(double2* tw, int M) {
 fks_status build_tables(Ctx& c) {
   const double pi = 3.14159265358979323846;
   const fks_params& p = c.p;
-  if (p.kernel == FKS_KERNEL_MAXWELL && p.M_radial > kMaxRadial) {
+  if (p.kernel != FKS_KERNEL_HARD_SPHERES && p.M_radial > kMaxRadial) {
     set_error("M_radial must be <= 64");
     return FKS_ERR_UNSUPPORTED;
   }
@@ -156,11 +156,18 @@ fks_status build_tables(Ctx& c) {
       c.w[d] = wt[i];
     }
   // radial rule (Maxwell molecules) and theta rule on [0, pi/2]
-  int Mr = p.kernel == FKS_KERNEL_MAXWELL ? p.M_radial : 1;
+  int Mr = p.kernel != FKS_KERNEL_HARD_SPHERES ? p.M_radial : 1;
   std::vector<double> rho, Wr, cij(Mr * (size_t)Mr, 0.0);
   gauss_legendre(Mr, 0.0, c.Rc, rho, Wr);
+  // b_t = 2 sum_j cij J0(rho_j tau) = 2 pi sum_j W_j rho_j B~(rho_i, rho_j) J0:  cij = pi W_j rho_j B~(rho_i, rho_j)
+  //   Maxwell molecules B~ = (1/pi)(rho_i^2 + rho_j^2)^(-1/2);  VHS B~ = 4 C_a (rho_i^2 + rho_j^2)^((a-1)/2) (A30)
+  const double vhs_C = p.vhs_C > 0.0 ? p.vhs_C : 1.0 / (4.0 * pi);
   for (int i = 0; i < Mr; i++)
-    for (int j = 0; j < Mr; j++) cij[i * Mr + j] = Wr[j] * rho[j] / std::sqrt(rho[i] * rho[i] + rho[j] * rho[j]);
+    for (int j = 0; j < Mr; j++) {
+      const double r2 = rho[i] * rho[i] + rho[j] * rho[j];
+      cij[i * Mr + j] = p.kernel == FKS_KERNEL_VHS ? pi * Wr[j] * rho[j] * 4.0 * vhs_C * std::pow(r2, (p.vhs_alpha - 1.0) / 2.0)
+                                                   : Wr[j] * rho[j] / std::sqrt(r2);
+    }
   std::vector<double> th, thw, thc(kThetaNodes);
   gauss_legendre(kThetaNodes, 0.0, 0.5 * pi, th, thw);
   for (int q = 0; q < kThetaNodes; q++) thc[q] = std::cos(th[q]);

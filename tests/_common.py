@@ -13,9 +13,10 @@ TOL_TABLE = 1e-13   # DESIGN.md P17
 
 
 @functools.lru_cache(maxsize=None)
-def oracle_tables(N, L, M, M_r, kernel, n_theta=0, n_phi=0, rule=0, cutoff_ratio=1.0):
+def oracle_tables(N, L, M, M_r, kernel, n_theta=0, n_phi=0, rule=0, cutoff_ratio=1.0, alpha=0.5,
+                  C_alpha=o.VHS_C_DEFAULT):
     return o.build_tables(N, L, M=M, M_r=M_r, kernel=kernel, n_theta=n_theta, n_phi=n_phi, rule=rule,
-                          cutoff_ratio=cutoff_ratio)
+                          cutoff_ratio=cutoff_ratio, alpha=alpha, C_alpha=C_alpha)
 
 
 def cfg_tables(name):

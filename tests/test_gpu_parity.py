@@ -113,6 +113,44 @@ def test_collision_aliased_N32_P32(cuda_device):
     assert rel_err_per_cell(Q, ref).max() <= TOL_Q
 
 
+# ---------------- variable hard spheres ----------------------------------------
+
+@pytest.mark.parametrize("alpha,C", [(0.5, 0.0), (0.3, 0.1), (1.0, 0.25)])
+def test_tables_vhs(cuda_device, alpha, C):
+    col = B.Collision(12, L_BOX, 16, 8, 2, vhs_alpha=alpha, vhs_C=C)
+    ref = oracle_tables(12, L_BOX, 16, 8, 2, alpha=alpha, C_alpha=C or o.VHS_C_DEFAULT)
+    a, b, _, _ = B.fks_get_tables(col.h, 12, ref.w.size)
+    assert np.abs(a - ref.a).max() <= TOL_TABLE * np.abs(ref.a).max()
+    assert np.abs(b - ref.b).max() <= TOL_TABLE * np.abs(ref.b).max()
+
+
+@pytest.mark.parametrize("N", [6, 8])
+def test_collision_vhs_vs_direct_sum(cuda_device, N):
+    f = inputs.random_field(3, N, seed=70 + N, signed=False).to(cuda_device)
+    col = B.Collision(N, L_BOX, 16, 4, 2, vhs_alpha=0.5)
+    Q = col.collision_batch(f).cpu().numpy()
+    tb = oracle_tables(N, L_BOX, 16, 4, 2, alpha=0.5)
+    ref = np.stack([o.collision_direct(x, tb) for x in f.cpu().numpy()])
+    assert rel_err_per_cell(Q, ref).max() <= TOL_Q
+
+
+def test_collision_vhs_fast_path_c2(cuda_device):
+    cfg = CONFIGS["c2"]
+    f = inputs.make_f(cfg, device=cuda_device, cells=[3])
+    col = B.Collision(cfg.N, cfg.L, cfg.M, 2, 2, vhs_alpha=0.5)
+    assert col.info["path"] == B.FKS_PATH_FAST and col.info["T"] == cfg.M * 2
+    Q = col.collision_batch(f).cpu().numpy()
+    ref = oracle_Q(f.cpu().numpy(), oracle_tables(cfg.N, cfg.L, cfg.M, 2, 2, alpha=0.5))
+    assert rel_err_per_cell(Q, ref).max() <= TOL_Q
+
+
+def test_vhs_argument_checks(cuda_device):
+    with pytest.raises(B.FksError):
+        B.Collision(8, L_BOX, 16, 4, 2, vhs_alpha=1.5)
+    with pytest.raises(B.FksError):
+        B.Collision(8, L_BOX, 16, 0, 2, vhs_alpha=0.5)
+
+
 def test_collision_bkw_report(cuda_device):
     """c1 (BKW, N = 24): Q vs the analytic ∂f/∂t.  Resolution-limited (~0.2-0.5, P14): reported,
     gated only loosely; the 1e-6 BKW pin is the oracle's N = 64 test."""
