@@ -12,7 +12,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libfks.so")
 
 FKS_OK, FKS_ERR_INVALID, FKS_ERR_UNSUPPORTED, FKS_ERR_NOMEM, FKS_ERR_CUDA, FKS_ERR_STATE = range(6)
-FKS_KERNEL_HARD_SPHERES, FKS_KERNEL_MAXWELL = 0, 1
+FKS_KERNEL_HARD_SPHERES, FKS_KERNEL_MAXWELL, FKS_KERNEL_VHS = 0, 1, 2
 FKS_QUAD_GL_UNIFORM, FKS_QUAD_PAPER_RECT = 0, 1
 FKS_PATH_AUTO, FKS_PATH_GENERIC, FKS_PATH_FAST = 0, 1, 2
 
