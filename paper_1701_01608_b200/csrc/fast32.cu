@@ -651,15 +651,7 @@ __global__ void __launch_bounds__(2 * NT, 1) hot_kernel_t12(Args A) {
 namespace v4 {
 constexpr int TM = 12;                        // CTAs (members) per team = per cell
 constexpr int PLN = P / TM;                   // 4 z-planes per member
-#ifndef V4_NB
-#define V4_NB 4
-#endif
-#ifndef V4_PUB
-#define V4_PUB 2
-#endif
-constexpr int NB = V4_NB;                     // W1 team buffers (Z warps run ahead by < NB terms)
-constexpr int PUB = V4_PUB;                   // W1 is published PUB terms at a time (one store drain per PUB terms)
-static_assert(PUB >= 1 && PUB <= NB, "publication batches must fit the W1 ring");
+constexpr int NB = 4;                         // W1 team buffers (Z warps run ahead by < NB terms)
 // V4_G6 = 1: 16 warps (2 YX groups of 6 + 4 Z warps, <= 128 registers)
 // V4_G4 = 1: 12 warps (2 YX groups of 4 + 4 Z warps, <= 168 registers); both 0: 8 warps (groups of 3 + 2 Z warps)
 #ifndef V4_G6
@@ -692,15 +684,6 @@ constexpr int GW = 3;
 #define V4_NZW 2
 #endif
 #endif
-// V4_ZT = 1 (with XP): the Z warps keep their f^ elements in TMEM (48 columns per lane, loaded once per cell) and
-// the member's table block of term t+1 is bulk-copied into shared memory while term t's class tasks run
-// V4_DBG_SKIP (timing experiments only, wrong results): bit 0 skips the YX transforms, bit 1 the Z work
-#ifndef V4_DBG_SKIP
-#define V4_DBG_SKIP 0
-#endif
-#ifndef V4_ZT
-#define V4_ZT 0
-#endif
 constexpr int NYX = 2 * GW, NZW = V4_NZW;     // YX warps (2 groups of GW), Z warps
 constexpr int NTHR = 32 * (NYX + NZW);        // 288
 constexpr int NZT = 32 * NZW;                 // Z threads
@@ -718,7 +701,7 @@ constexpr int PLANE_B = W1IN_B + NYSLOT * YBUF_B;  // per owned plane
 constexpr int ZBLK_B = K * MAXH * 16;         // 20336 B
 constexpr int OFF_Z = PLN * PLANE_B;          // 124992
 constexpr int SMEM_B = OFF_Z + 3 * ZBLK_B;    // Z: products (2) + the cell's f^ block (tables are read from L2)
-constexpr int CTR_STRIDE = 64 * NB;           // counter words per team (one 128-B line per counter)
+constexpr int CTR_STRIDE = 256;               // counter words per team (one 128-B line per counter)
 // Synchronisation (exact because buffer b = tg % NB is refilled only after all consumers of its previous
 // generation acknowledged it):  W1(tg) is complete when zcnt[b] == TM (tg / NB + 1);  buffer b may be
 // overwritten with W1(tg) when ycnt[b] == 2 TM (tg / NB)  (2 YX groups per member).
@@ -880,16 +863,6 @@ __device__ __forceinline__ void tmem_ld16_async(uint32_t addr, uint32_t (&v)[16]
       : "r"(addr));
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
-__device__ __forceinline__ void tmem_ld8_async(uint32_t addr, uint32_t (&v)[8]) {
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
-               : "r"(addr));
-}
-__device__ __forceinline__ void tmem_st8(uint32_t addr, const uint32_t (&v)[8]) {
-  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
-               ::"r"(addr), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
-               : "memory");
-}
 
 __device__ __forceinline__ void g_accumulate(uint32_t tcol, const double2 (&u)[16]) {
   uint32_t gw[32];
@@ -922,7 +895,6 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
   unsigned* ycnt = zcnt + 32 * NB;                         // + 32 b
   const long long ncell_team = (team < A.n_cells) ? (A.n_cells - 1 - team) / A.nteams + 1 : 0;
   const long long total_tg = ncell_team * A.T1;
-  const long long dbg_cell = (team + 2LL * A.nteams < A.n_cells) ? team + 2LL * A.nteams : team;
 
   if (warp == 0) {
 #if V4_G6 && V4_XP
@@ -1012,9 +984,8 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
 #pragma unroll 1
       for (int t = 0; t < A.T1; t++, tg++) {
         const int T = (int)tg;
-        // phase stamps (steady state: the team's third cell): Y warp (g,c) = (0,0) slots 0-2, X warp (0,0) 3-6
-        long long* st = (A.dbg && lane == 0 && (warp == 6 || warp == 0) && cell == dbg_cell && t >= 2 && t < 6)
-                            ? A.dbg + (long long)blockIdx.x * 128 + (t - 2) * 16 + (warp == 0 ? 3 : 0) : nullptr;
+        long long* st = (A.dbg && lane == 0 && warp == 6 && cell == team && t >= 2 && t < 6)
+                            ? A.dbg + (long long)blockIdx.x * 128 + (t - 2) * 16 : nullptr;
         if (st) st[0] = clock64();
         if (!isx) {
           // ---------------- Y warp ----------------
@@ -1027,7 +998,7 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
           if (st) st[1] = clock64();
           wait_ge(&xc[c], T);  // slot c: X(g, c) of term t-1 has parked its rows
 #pragma unroll 1
-          for (int pl = 0; pl < (V4_DBG_SKIP & 1 ? 0 : 2); pl++) {
+          for (int pl = 0; pl < 2; pl++) {
             double2 u[16];
             xform48((pl ? in1 : in0) + (lane < K ? lane : K - 1) * K, 1, c, u);
             if (lane < K) {
@@ -1046,7 +1017,6 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
         } else {
           // ---------------- X warp ----------------
           wait_ge(&yc[c], T + 1);
-          if (st) st[1] = clock64();
           if (t == 0) {  // first term of the cell: zero the three G blocks
             uint32_t zw[32];
 #pragma unroll
@@ -1054,7 +1024,7 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
 #pragma unroll 1
             for (int rx = 0; rx < 3; rx++) tmem_st32(tX + 32u * rx, zw);
           }
-          if (!(V4_DBG_SKIP & 1)) {  // park the row (31 complex = 124 words) in this lane's TMEM columns, 8 per store
+          {  // park the row (31 complex = 124 words) in this lane's TMEM columns, 8 values per store
             const double2* row = ybuf(xp, c) + xq * K;
 #pragma unroll
             for (int ch = 0; ch < 4; ch++) {
@@ -1077,9 +1047,8 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
             __threadfence_block();
             atomicAdd(&xc[c], 1);  // the Y slot may be refilled
           }
-          if (st) st[2] = clock64();
 #pragma unroll 1
-          for (int rx = 0; rx < (V4_DBG_SKIP & 1 ? 0 : 3); rx++) {
+          for (int rx = 0; rx < 3; rx++) {
             double2 u[16];
             const double sg = (rx == 1) ? -0.86602540378443864676 : 0.86602540378443864676;
 #pragma unroll
@@ -1112,7 +1081,6 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
             g_accumulate(tX + 32u * rx, u);
           }
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-          if (st) st[3] = clock64();
           if (t == A.T1 - 1) {  // G[cell][px = 3q' + rx][pz][py = 3 xq + c]
             double* Gc = A.G + cell * (long long)(P * P * P) + (long long)(pz0 + xp) * P;
 #pragma unroll 1
@@ -1386,92 +1354,6 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
     const int zt = tid - 32 * NYX;  // 0..NZT-1
     double2* zp = reinterpret_cast<double2*>(smem + OFF_Z);
     double2* zm = reinterpret_cast<double2*>(smem + OFF_Z + ZBLK_B);
-#if V4_ZT
-    // element pairs {i, 30 - i} of pencil j, e = i * nh + j (e = zt + u NZT, u < ZIT, one fixed set per thread);
-    // i = e / nh by multiply-high (exact: e nh < 2^32).  f^ of the thread's elements lives in TMEM columns
-    // 448 + 8u of its lane (loaded once per cell); the table block of the term is in shared memory (TMA).
-    constexpr int ZIT = (16 * MAXH + NZT - 1) / NZT;
-    static_assert(ZIT * 8 <= 64 && 16 * MAXH <= ZIT * NZT, "Z element map");
-    double2* tabs = reinterpret_cast<double2*>(smem + OFF_Z + 2 * ZBLK_B);  // table block of the current term
-    const uint32_t tF = tbase + ((uint32_t)(32 * (warp & 3)) << 16) + 448u;
-    const uint32_t tblk = (uint32_t)(K * nh) * 16u;
-    const unsigned mdiv = 0xffffffffu / (unsigned)nh + 1u;
-    const int ne = 16 * nh;
-    auto issue_tab = [&](int tt) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_expect(&bar_tab, tblk);
-      bulk_g2s(tabs, A.tabT + (long long)tt * LHN + K * h0, tblk, &bar_tab);
-    };
-    if (zt == 0 && ncell_team > 0) issue_tab(0);
-    uint32_t par_tab = 0;
-    long long tg = 0;
-#pragma unroll 1
-    for (long long cell = team; cell < A.n_cells; cell += A.nteams) {
-      {  // this thread's f^ elements -> TMEM
-        const double2* fg = A.fhatT + cell * (long long)LHN + K * h0;
-#pragma unroll
-        for (int u = 0; u < ZIT; u++) {
-          const int e = min(zt + u * NZT, ne - 1);
-          const int i = (int)__umulhi((unsigned)e, mdiv), j = e - i * nh;
-          const double2 f1 = __ldg(fg + i * nh + j), f2 = __ldg(fg + (30 - i) * nh + j);
-          uint32_t w[8] = {(uint32_t)__double2loint(f1.x), (uint32_t)__double2hiint(f1.x),
-                           (uint32_t)__double2loint(f1.y), (uint32_t)__double2hiint(f1.y),
-                           (uint32_t)__double2loint(f2.x), (uint32_t)__double2hiint(f2.x),
-                           (uint32_t)__double2loint(f2.y), (uint32_t)__double2hiint(f2.y)};
-          tmem_st8(tF + 8u * u, w);
-        }
-        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-      }
-#pragma unroll 1
-      for (int t = 0; t < A.T1; t++, tg++) {
-        long long* st = (A.dbg && zt == 0 && cell == dbg_cell && t >= 2 && t < 6)
-                            ? A.dbg + (long long)blockIdx.x * 128 + (t - 2) * 16 + 8 : nullptr;
-        if (st) st[0] = clock64();
-        mbar_wait(&bar_tab, par_tab);
-        par_tab ^= 1;
-        if (st) st[1] = clock64();
-        // products: Z = (a + ib) f^ for the staged pencils, and for their mirrors (-lx,-ly): (a + ib) conj(f^)
-        // at the reversed lz (a, b even; f real)
-        {
-          const double2* __restrict__ tr = tabs;
-          double2* __restrict__ pw = zp;
-          double2* __restrict__ mw = zm;
-#pragma unroll
-          for (int hh = 0; hh < ZIT; hh += 3) {
-            uint32_t fw[3][8];
-            double2 a1[3], a2[3];
-            int o1[3], o2[3];
-#pragma unroll
-            for (int u = 0; u < 3; u++) {
-              if (hh + u < ZIT) tmem_ld8_async(tF + 8u * (hh + u), fw[u]);
-              const int e = min(zt + (hh + u) * NZT, ne - 1);
-              const int i = (int)__umulhi((unsigned)e, mdiv), j = e - i * nh;
-              o1[u] = i * nh + j;
-              o2[u] = (30 - i) * nh + j;
-              a1[u] = tr[o1[u]];
-              a2[u] = tr[o2[u]];
-            }
-            tmem_wait_ld();
-#pragma unroll
-            for (int u = 0; u < 3; u++) {
-              if (hh + u >= ZIT || zt + (hh + u) * NZT >= ne) continue;
-              const double2 f1 = make_double2(__hiloint2double((int)fw[u][1], (int)fw[u][0]),
-                                              __hiloint2double((int)fw[u][3], (int)fw[u][2]));
-              const double2 f2 = make_double2(__hiloint2double((int)fw[u][5], (int)fw[u][4]),
-                                              __hiloint2double((int)fw[u][7], (int)fw[u][6]));
-              pw[o1[u]] = make_double2(fma(a1[u].x, f1.x, -a1[u].y * f1.y), fma(a1[u].x, f1.y, a1[u].y * f1.x));
-              pw[o2[u]] = make_double2(fma(a2[u].x, f2.x, -a2[u].y * f2.y), fma(a2[u].x, f2.y, a2[u].y * f2.x));
-              mw[o1[u]] = make_double2(fma(a2[u].x, f2.x, a2[u].y * f2.y), fma(-a2[u].x, f2.y, a2[u].y * f2.x));
-              mw[o2[u]] = make_double2(fma(a1[u].x, f1.x, a1[u].y * f1.y), fma(-a1[u].x, f1.y, a1[u].y * f1.x));
-            }
-          }
-        }
-        nbar(3, NZT);  // products complete: the table buffer is free for the next term
-        if (zt == 0) {
-          if (t + 1 < A.T1) issue_tab(t + 1);
-          else if (cell + A.nteams < A.n_cells) issue_tab(0);
-        }
-#else
     double2* fh = reinterpret_cast<double2*>(smem + OFF_Z + 2 * ZBLK_B);  // the cell's f^ block (TMA, per cell)
     const uint32_t fblk = (uint32_t)(K * nh) * 16u;
     auto issue_fh = [&](long long cl) {
@@ -1489,7 +1371,7 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
 #pragma unroll 1
       for (int t = 0; t < A.T1; t++, tg++) {
         const double2* tb = A.tabT + (long long)t * LHN + K * h0;     // the member's table block (L2)
-        long long* st = (A.dbg && zt == 0 && cell == dbg_cell && t >= 2 && t < 6)
+        long long* st = (A.dbg && zt == 0 && cell == team && t >= 2 && t < 6)
                             ? A.dbg + (long long)blockIdx.x * 128 + (t - 2) * 16 + 8 : nullptr;
         if (st) st[0] = clock64();
         if (st) st[1] = clock64();
@@ -1506,7 +1388,7 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
           // every load of this thread (<= ZIT iterations) is issued before the first product: one L2 round trip
           constexpr int ZIT = (16 * MAXH + NZT - 1) / NZT;  // all table loads of this thread in one L2 round
 #pragma unroll 1
-          for (int zb = 0; zb * ZIT * NZT < (V4_DBG_SKIP & 2 ? 0 : ne); zb++) {
+          for (int zb = 0; zb * ZIT * NZT < ne; zb++) {
           const int zt0 = zt + zb * ZIT * NZT;
           double2 f1[ZIT], a1[ZIT], f2[ZIT], a2[ZIT];
           int o1[ZIT], o2[ZIT];
@@ -1534,13 +1416,12 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
         }
         nbar(3, NZT);  // products complete (after the cell's last term the f^ block is free)
         if (zt == 0 && t == A.T1 - 1 && cell + A.nteams < A.n_cells) issue_fh(cell + A.nteams);
-#endif
         // publish W1(tg - 2) and W1(tg - 1) every second term: one store drain per pair (it costs ~1.4 K cycles
         // on the Z warps, which set the period; the consumers have slack)
-        if (zt == 0 && tg >= PUB && tg % PUB == 0) {
+        if (zt == 0 && tg >= 2 && (tg & 1) == 0) {
           __threadfence();
-#pragma unroll 1
-          for (long long tp = tg - PUB; tp < tg; tp++) atomicAdd(zcnt + 32 * (tp % NB), 1u);
+          atomicAdd(zcnt + 32 * ((tg - 2) % NB), 1u);
+          atomicAdd(zcnt + 32 * ((tg - 1) % NB), 1u);
         }
         if (st) st[2] = clock64();
         if (zt == 0) {
@@ -1553,7 +1434,7 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
         {  // 4 Z warps: single class tasks tau = r * na + j, 2 rounds of 128 threads cover 3 na <= 246
           const int na = nh + nmir;
 #pragma unroll 1
-          for (int kk = zt; kk < (V4_DBG_SKIP & 2 ? 0 : 2 * NZT); kk += NZT) {
+          for (int kk = zt; kk < 2 * NZT; kk += NZT) {
             if (kk - lane >= 3 * na) break;  // no active lane in this warp (warp-uniform)
             const bool act = kk < 3 * na;
             const int kc = act ? kk : 0;
@@ -1600,10 +1481,10 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
         if (st) st[4] = clock64();
       }
     }
-    if (zt == 0 && tg > 0) {  // publish what is left: W1(PUB floor((tg-1)/PUB)) .. W1(tg-1)
+    if (zt == 0 && tg > 0) {  // publish what is left (tg even: W1(tg-2), W1(tg-1); tg odd: W1(tg-1))
       __threadfence();
-#pragma unroll 1
-      for (long long tp = ((tg - 1) / PUB) * PUB; tp < tg; tp++) atomicAdd(zcnt + 32 * (tp % NB), 1u);
+      if ((tg & 1) == 0 && tg >= 2) atomicAdd(zcnt + 32 * ((tg - 2) % NB), 1u);
+      atomicAdd(zcnt + 32 * ((tg - 1) % NB), 1u);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");

@@ -24,16 +24,15 @@ raw = buf[: 144 * 128].reshape(144, 8, 16)[:, :4, :]  # [cta][term][slot]
 raw = raw[raw[:, 0, 0] > 0]
 yx, z = raw[:, :, :8].astype(float), raw[:, :, 8:].astype(float)
 print("CTAs sampled:", len(raw))
-for name, a, b in [("Y(0,0): wait W1 (poll + TMA)", 0, 1), ("Y(0,0): wait slot + 2 transforms", 1, 2),
-                   ("X(0,0): wait Y", 3, 4), ("X(0,0): park rows", 4, 5), ("X(0,0): 3 transforms + G", 5, 6)]:
+for name, a, b in [("YX: wait W1 (poll + TMA)", 0, 1), ("YX: R1 (Y0,Y0,Y1)", 1, 2), ("YX: R2 (X c=0)", 2, 3),
+                   ("YX: R3 (Y1,Y2,Y2)", 3, 4), ("YX: R4+R5 (X c=1,2)", 4, 5)]:
     d = yx[:, :, b] - yx[:, :, a]
-    print(f"{name:34s} median {np.median(d):8.0f}  p10 {np.percentile(d, 10):8.0f}  p90 {np.percentile(d, 90):8.0f}")
-for name, col in [("Y term period", 0), ("X term period", 3)]:
-    d = yx[:, 1:, col] - yx[:, :-1, col]
-    print(f"{name:34s} median {np.median(d):8.0f}")
+    print(f"{name:28s} median {np.median(d):8.0f}  p10 {np.percentile(d, 10):8.0f}  p90 {np.percentile(d, 90):8.0f}")
+d = yx[:, 1:, 0] - yx[:, :-1, 0]
+print(f"{'YX term period':28s} median {np.median(d):8.0f}")
 for name, a, b in [("Z: wait tab", 0, 1), ("Z: products", 1, 2), ("Z: wait W1 buffer free", 2, 3),
                    ("Z: class tasks + stores", 3, 4)]:
     d = z[:, :, b] - z[:, :, a]
-    print(f"{name:34s} median {np.median(d):8.0f}  p10 {np.percentile(d, 10):8.0f}  p90 {np.percentile(d, 90):8.0f}")
+    print(f"{name:28s} median {np.median(d):8.0f}  p10 {np.percentile(d, 10):8.0f}  p90 {np.percentile(d, 90):8.0f}")
 d = z[:, 1:, 0] - z[:, :-1, 0]
-print(f"{'Z term period':34s} median {np.median(d):8.0f}")
+print(f"{'Z term period':28s} median {np.median(d):8.0f}")
