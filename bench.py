@@ -462,6 +462,7 @@ def main():
                                      "(ncu --set full of this kernel in this bench command), scaled to cells per launch",
                      "kernel": "term loop (a3-a5: table product, pruned 3D inverse, gain-loss accumulate)",
                      "flop_per_cell": fl["hot"], "cells_per_launch": cells_per_launch, "ms_per_launch": hot_ms,
+                     "frac_of_measured_dfma": achieved / 33.613,
                      "peak_note": "FP64 DFMA: 148 SM x 64 lanes x 2 flop x 1965 MHz (unit counts, max clock); "
                                   "measured DFMA microbench 33.6 TF/s (profiles/r01_box_microbench.jsonl)"},
         "whole_step": {"flop_per_cell": fl["total"],
