@@ -213,9 +213,10 @@ def run_bgk(args):
     from paper_1701_01608_b200 import binding as B
     from paper_1701_01608_b200 import inputs
     if ws > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", init_method="env://")
-    dev = torch.device("cuda", local if ws > 1 else 0)
+        torch.cuda.set_device(local % torch.cuda.device_count())
+        # FKS_BENCH_BACKEND=gloo only to exercise the multi-rank flow where the ranks share one GPU (no timing claim)
+        dist.init_process_group(os.environ.get("FKS_BENCH_BACKEND", "nccl"), init_method="env://")
+    dev = torch.device("cuda", local % torch.cuda.device_count() if ws > 1 else 0)
     torch.cuda.set_device(dev)
     stream = torch.cuda.current_stream(dev)
     col = B.Collision(cfg.N, cfg.L, cfg.M, cfg.M_r, cfg.kernel)
@@ -352,9 +353,10 @@ def main():
     from paper_1701_01608_b200 import inputs
 
     if ws > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", init_method="env://")
-    dev = torch.device("cuda", local if ws > 1 else 0)
+        torch.cuda.set_device(local % torch.cuda.device_count())
+        # FKS_BENCH_BACKEND=gloo only to exercise the multi-rank flow where the ranks share one GPU (no timing claim)
+        dist.init_process_group(os.environ.get("FKS_BENCH_BACKEND", "nccl"), init_method="env://")
+    dev = torch.device("cuda", local % torch.cuda.device_count() if ws > 1 else 0)
     torch.cuda.set_device(dev)
     stream = torch.cuda.current_stream(dev)
 

@@ -35,6 +35,8 @@ def max_over_ranks(x: float, device=None) -> float:
     import torch.distributed as dist
     if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
         return float(x)
+    if dist.get_backend() == "gloo":
+        device = None  # host tensor for the CPU backend
     t = torch.tensor([float(x)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
