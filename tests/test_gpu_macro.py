@@ -178,3 +178,48 @@ def test_bgk_step_c3_full_size_sampled(cuda_device):
     # mass over the periodic box: transport permutes, relaxation changes it only by the quadrature error of E
     m_in, m_out = f.sum().item(), out.sum().item()
     assert abs(m_out - m_in) <= 1e-6 * abs(m_in)
+
+
+def test_abi_rejects_invalid_arguments(cuda_device):
+    """Validation errors of the moments / BGK / slab entry points return before any launch (fks.h conventions)."""
+    import ctypes
+    lib = B.load_library()
+    N = 8
+    col = B.Collision(N, 4.0, 16, 16, 0)
+    f = torch.rand(3, N, N, N, dtype=torch.float64, device=cuda_device)
+    g = torch.empty_like(f)
+    U = torch.empty(3, 5, dtype=torch.float64, device=cuda_device)
+    h = col.h
+    ST = lambda fn, *a: fn(*a)  # noqa: E731
+    inv, state = B.FKS_ERR_INVALID, B.FKS_ERR_STATE
+    # NULL handle
+    assert ST(lib.fks_moments, None, f.data_ptr(), U.data_ptr(), None, 3, None) == inv
+    assert ST(lib.fks_bgk_batch, None, f.data_ptr(), g.data_ptr(), 1.0, 3, None) == inv
+    # moments: both outputs NULL, negative count, host pointer, output overlapping the input
+    assert ST(lib.fks_moments, h, f.data_ptr(), None, None, 3, None) == inv
+    assert ST(lib.fks_moments, h, f.data_ptr(), U.data_ptr(), None, -1, None) == inv
+    fh = torch.zeros(3, N, N, N, dtype=torch.float64)
+    assert ST(lib.fks_moments, h, fh.data_ptr(), U.data_ptr(), None, 3, None) == inv
+    assert ST(lib.fks_moments, h, f.data_ptr(), f.data_ptr(), None, 3, None) == inv
+    # BGK operator: overlap, non-finite nu
+    assert ST(lib.fks_bgk_batch, h, f.data_ptr(), f.data_ptr(), 1.0, 3, None) == inv
+    assert ST(lib.fks_bgk_batch, h, f.data_ptr(), g.data_ptr(), float("nan"), 3, None) == inv
+    # BGK step before any transport setup; slab calls on a single-domain handle
+    assert ST(lib.fks_bgk_step, h, f.data_ptr(), g.data_ptr(), 0.1, None, None, None) == state
+    H = ctypes.c_int()
+    assert ST(lib.fks_slab_halo, h, ctypes.byref(H)) == state
+    col.transport_setup((3, 1, 1), 1, 1)
+    assert ST(lib.fks_bgk_step, h, f.data_ptr(), f.data_ptr(), 0.1, None, None, None) == inv
+    planes = (ctypes.c_void_p * 8)()
+    assert ST(lib.fks_step_slab, h, planes, g.data_ptr(), 0.01, None) == state
+    # slab setup: invalid ranges; then the single-domain step is refused and a NULL plane is rejected
+    assert ST(lib.fks_transport_setup_slab, h, 4, 1, 1, -1, 2, 1, 1) == inv
+    assert ST(lib.fks_transport_setup_slab, h, 4, 1, 1, 0, 0, 1, 1) == inv
+    assert ST(lib.fks_transport_setup_slab, h, 4, 1, 1, 0, 2, 1, 1) == B.FKS_OK
+    assert ST(lib.fks_bgk_step, h, f.data_ptr(), g.data_ptr(), 0.1, None, None, None) == state
+    assert ST(lib.fks_step_slab, h, None, g.data_ptr(), 0.01, None) == inv
+    assert ST(lib.fks_step_slab, h, planes, g.data_ptr(), 0.01, None) == inv  # NULL entries
+    # the handle still works after all the rejected calls
+    col.transport_setup((3, 1, 1), 1, 1)
+    col.bgk_step(f, g, 0.1)
+    B.fks_sync(h)
