@@ -446,6 +446,14 @@ def main():
         e2e = {"value": cells_all * cfg.N ** 3 * args.e2e_steps / dt, "unit": unit,
                "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes, "steps": args.e2e_steps,
                "api": "fks_step_host (pinned host buffers)"}
+        # the collision operator alone through the host-buffer call (BASELINE's Q(f,f) metric end to end)
+        B.fks_collision_batch_host(col.h, hin, hout, cfg.n_cells)  # warm-up
+        barrier()
+        t0 = time.perf_counter()
+        B.fks_collision_batch_host(col.h, hin, hout, cfg.n_cells)
+        dt = D.max_over_ranks(time.perf_counter() - t0, dev)
+        e2e["collision_only"] = {"value": cells_all * cfg.N ** 3 / dt, "unit": unit,
+                                 "api": "fks_collision_batch_host (pinned host buffers)"}
         del hin, hout
 
     if rank != 0:

@@ -436,12 +436,38 @@ fks_status fks_collision_batch_host(fks_ctx* h, const double* f_host, double* Q_
   fks_status rc;
   if ((rc = sticky_check())) return rc;
   if ((rc = ensure_stage(c, n_cells))) return rc;
-  const size_t bytes = (size_t)n_cells * c.N * c.N * c.N * sizeof(double);
+  // pipelined in chunks of cells over three streams: copy-in of chunk i+1 and copy-out of chunk i-1 overlap the
+  // collision of chunk i (cells are independent)
+  if (!c.h2d_stream) cudaStreamCreateWithFlags(&c.h2d_stream, cudaStreamNonBlocking);
+  if (!c.d2h_stream) cudaStreamCreateWithFlags(&c.d2h_stream, cudaStreamNonBlocking);
+  const long long nv = (long long)c.N * c.N * c.N;
+  const long long nch = std::max(1LL, std::min(32LL, n_cells / 512));
   cudaStream_t st = c.stage_stream;
-  if ((rc = cuda_status(cudaMemcpyAsync(c.d_stage_in, f_host, bytes, cudaMemcpyHostToDevice, st), "H2D"))) return rc;
-  if ((rc = run_collision(c, c.d_stage_in, c.d_stage_out, n_cells, false, 0.0, st))) return rc;
-  if ((rc = cuda_status(cudaMemcpyAsync(Q_host, c.d_stage_out, bytes, cudaMemcpyDeviceToHost, st), "D2H"))) return rc;
-  return cuda_status(cudaStreamSynchronize(st), "host-buffer collision");
+  std::vector<cudaEvent_t> eh(nch), ec(nch);
+  for (long long i = 0; i < nch; i++) {
+    cudaEventCreateWithFlags(&eh[i], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ec[i], cudaEventDisableTiming);
+  }
+  for (long long i = 0; i < nch && !rc; i++) {
+    const long long c0 = n_cells * i / nch, m = n_cells * (i + 1) / nch - c0;
+    rc = cuda_status(cudaMemcpyAsync(c.d_stage_in + c0 * nv, f_host + c0 * nv, (size_t)m * nv * sizeof(double),
+                                     cudaMemcpyHostToDevice, c.h2d_stream), "H2D");
+    if (!rc) rc = cuda_status(cudaEventRecord(eh[i], c.h2d_stream), "event");
+  }
+  for (long long i = 0; i < nch && !rc; i++) {
+    const long long c0 = n_cells * i / nch, m = n_cells * (i + 1) / nch - c0;
+    rc = cuda_status(cudaStreamWaitEvent(st, eh[i], 0), "wait H2D");
+    if (!rc) rc = run_collision(c, c.d_stage_in + c0 * nv, c.d_stage_out + c0 * nv, m, false, 0.0, st);
+    if (!rc) rc = cuda_status(cudaEventRecord(ec[i], st), "event");
+    if (!rc) rc = cuda_status(cudaStreamWaitEvent(c.d2h_stream, ec[i], 0), "wait compute");
+    if (!rc) rc = cuda_status(cudaMemcpyAsync(Q_host + c0 * nv, c.d_stage_out + c0 * nv, (size_t)m * nv * sizeof(double),
+                                              cudaMemcpyDeviceToHost, c.d2h_stream), "D2H");
+  }
+  fks_status rs = cuda_status(cudaStreamSynchronize(c.d2h_stream), "host-buffer collision");
+  cudaStreamSynchronize(st);
+  cudaStreamSynchronize(c.h2d_stream);
+  for (long long i = 0; i < nch; i++) { cudaEventDestroy(eh[i]); cudaEventDestroy(ec[i]); }
+  return rc ? rc : rs;
 }
 
 // Host-buffer step, pipelined over slabs of x-planes on three streams: the input planes are copied in (the

@@ -388,3 +388,21 @@ def test_step_host_pageable(cuda_device):
     B.fks_step_host(host.h, hin, hout, 0.02)
     torch.cuda.synchronize()
     assert torch.equal(out.cpu(), hout)
+
+
+@pytest.mark.parametrize("name,n", [("c0", 8), ("c2", 1536)])
+def test_collision_batch_host_matches_device(cuda_device, name, n):
+    """fks_collision_batch_host (pinned host buffers, chunks pipelined over three streams) equals the
+    device-resident batch bit for bit (cells are independent; each chunk runs the same kernels)."""
+    cfg = CONFIGS[name]
+    f = inputs.make_f(cfg, device=cuda_device, cells=[c % cfg.n_cells for c in range(n)])
+    col = make(cfg)
+    Qd = col.collision_batch(f).cpu()
+    fh = f.cpu().pin_memory()
+    Qh = torch.empty_like(fh).pin_memory()
+    B.fks_collision_batch_host(col.h, fh, Qh, n)
+    assert torch.equal(Qh, Qd)
+    fp = f.cpu()  # pageable
+    Qp = torch.empty_like(fp)
+    B.fks_collision_batch_host(col.h, fp, Qp, n)
+    assert torch.equal(Qp, Qd)
