@@ -88,8 +88,9 @@ fks_status fks_collision_init_ex(fks_ctx** out, const fks_params* p);
  * Q must not overlap f. */
 fks_status fks_collision_batch(fks_ctx* h, const double* f, double* Q, long long n_cells, void* stream);
 
-/* Same operation on HOST buffers: copies f to the device, computes, copies Q back, in chunks; returns when
- * Q is written (synchronous).  Used for the end-to-end measurement. */
+/* Same operation on HOST buffers: chunks of cells (up to 32) are copied in, collided and copied back on three
+ * streams so that the copies overlap the compute; returns when Q is written (synchronous).  Bit-identical to
+ * fks_collision_batch.  Used for the end-to-end measurement. */
 fks_status fks_collision_batch_host(fks_ctx* h, const double* f_host, double* Q_host, long long n_cells);
 
 /* Configure the exact transport (A16): periodic nx*ny*nz cells of width dx, time step
@@ -105,7 +106,10 @@ fks_status fks_transport_step(fks_ctx* h, const double* f_in, double* f_out, voi
  * Euler: f_out = f* + coll_scale * Q(f*), f* = transported f_in, coll_scale = dt/Kn. */
 fks_status fks_step(fks_ctx* h, const double* f_in, double* f_out, double coll_scale, void* stream);
 
-/* Host-buffer variant of fks_step (synchronous), for the end-to-end measurement. */
+/* Host-buffer variant of fks_step (synchronous), for the end-to-end measurement.  The step is pipelined over
+ * x-slabs (one plane each, up to 32; env FKS_HOST_SLABS overrides) on three streams: copy-in (wrap-around halo
+ * first), transport + collision of each slab as soon as its source planes have landed, copy-out.  Pinned host
+ * buffers overlap fully; pageable ones work too.  Bit-identical to fks_step. */
 fks_status fks_step_host(fks_ctx* h, const double* f_in_host, double* f_out_host, double coll_scale);
 
 /* Slab decomposition in x for one process per GPU (the paper's MPI FKS).
