@@ -46,12 +46,18 @@ __global__ void __launch_bounds__(256) dft_axis_kernel(AxisArgs A) {
     const int vo = o - A.out_off;
     double sr = 0.0, si = 0.0;
     const long long base = b * A.n_in * A.R + r;
+    // twiddle index m_i = (sign (i - in_off) vo) mod M, advanced incrementally (no division in the loop); the
+    // table index of the input element stays within one cell along the axis
+    int step = (int)(((long long)A.sign * vo) % A.M);
+    if (step < 0) step += A.M;
+    int m = (int)(((long long)A.sign * (-A.in_off) * vo) % A.M);
+    if (m < 0) m += A.M;
+    const long long tab0 = (IK == IN_CPLX_TAB) ? base % A.cell_elems : 0;
     for (int i = 0; i < A.n_in; i++) {
-      long long e = base + (long long)i * A.R;
-      int m = (int)(((long long)(i - A.in_off) * vo) % A.M);
-      if (m < 0) m += A.M;
-      if (A.sign < 0 && m) m = A.M - m;
+      const long long e = base + (long long)i * A.R;
       const double2 w = A.tw[m];
+      m += step;
+      if (m >= A.M) m -= A.M;
       double xr, xi;
       if (IK == IN_REAL) {
         xr = reinterpret_cast<const double*>(A.in)[e];
@@ -60,7 +66,7 @@ __global__ void __launch_bounds__(256) dft_axis_kernel(AxisArgs A) {
         double2 x = reinterpret_cast<const double2*>(A.in)[e];
         xr = x.x; xi = x.y;
         if (IK == IN_CPLX_TAB) {
-          double2 t = A.ab[e % A.cell_elems];  // (a, b): (a + i b)(xr + i xi)
+          double2 t = A.ab[tab0 + (long long)i * A.R];  // (a, b): (a + i b)(xr + i xi)
           double zr = t.x * xr - t.y * xi, zi = t.x * xi + t.y * xr;
           xr = zr; xi = zi;
         }
