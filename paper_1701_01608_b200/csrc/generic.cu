@@ -53,6 +53,8 @@ __global__ void __launch_bounds__(256) dft_axis_kernel(AxisArgs A) {
     int m = (int)(((long long)A.sign * (-A.in_off) * vo) % A.M);
     if (m < 0) m += A.M;
     const long long tab0 = (IK == IN_CPLX_TAB) ? base % A.cell_elems : 0;
+    double sr1 = 0.0, si1 = 0.0;  // odd-i partial sums: two independent FMA chains
+#pragma unroll 2
     for (int i = 0; i < A.n_in; i++) {
       const long long e = base + (long long)i * A.R;
       const double2 w = A.tw[m];
@@ -71,11 +73,16 @@ __global__ void __launch_bounds__(256) dft_axis_kernel(AxisArgs A) {
           xr = zr; xi = zi;
         }
       }
-      sr = fma(xr, w.x, fma(-xi, w.y, sr));
-      si = fma(xr, w.y, fma(xi, w.x, si));
+      if (i & 1) {
+        sr1 = fma(xr, w.x, fma(-xi, w.y, sr1));
+        si1 = fma(xr, w.y, fma(xi, w.x, si1));
+      } else {
+        sr = fma(xr, w.x, fma(-xi, w.y, sr));
+        si = fma(xr, w.y, fma(xi, w.x, si));
+      }
     }
-    sr *= A.scale;
-    si *= A.scale;
+    sr = (sr + sr1) * A.scale;
+    si = (si + si1) * A.scale;
     if (OK == OUT_CPLX) {
       reinterpret_cast<double2*>(A.out)[idx] = make_double2(sr, si);
     } else if (OK == OUT_ACC_G) {
