@@ -1829,9 +1829,10 @@ bool fast_available(const Ctx& c) { return c.N == 32 && c.P == 48; }
 size_t xform32_ws_bytes_per_cell();
 cudaError_t xform32_prepare();
 void xform32_tables_lh(const double2* ab, double2* abL, int T1, int nb);
-void xform32_forward(Ctx& c, const double* fin, double2* fhT, double2* scratch, long long n, int nb, cudaStream_t st);
+void xform32_forward(Ctx& c, const double* fin, double2* fhT, double2* scratch, long long n, int nb, cudaStream_t st,
+                     const GatherSrc* gs);
 void xform32_back(Ctx& c, const double* G, double2* scratch_a, double2* scratch_b, const double* fin, double* out,
-                  long long n, bool euler, double s, cudaStream_t st);
+                  long long n, bool euler, double s, cudaStream_t st, const GatherSrc* gs);
 
 size_t fast_ws_bytes_per_cell(const Ctx&) { return xform32_ws_bytes_per_cell(); }
 
@@ -1919,14 +1920,14 @@ fks_status fast_prepare(Ctx& c) {
 }
 
 fks_status fast_collision(Ctx& c, const double* fin, double* out, long long n, bool euler, double s,
-                          cudaStream_t st) {
+                          cudaStream_t st, const GatherSrc* gs) {
   using namespace f32;
   // workspace: f^T [n][K^3] complex | scratch [n][P*K*16] complex | G [n][P^3] fp64
   double2* fhT = reinterpret_cast<double2*>(c.d_ws);
   double2* scratch = fhT + n * K * NPEN;
   double* G = reinterpret_cast<double*>(scratch + n * (long long)P * K * 16);
   c.prof.begin(1, st);
-  xform32_forward(c, fin, fhT, scratch, n, c.fast_variant, st);
+  xform32_forward(c, fin, fhT, scratch, n, c.fast_variant, st, gs);
   c.prof.end(1, st);
 
   c.prof.begin(2, st);
@@ -1969,7 +1970,7 @@ fks_status fast_collision(Ctx& c, const double* fin, double* out, long long n, b
   if (rc) return rc;
 
   c.prof.begin(3, st);
-  xform32_back(c, G, scratch, fhT, fin, out, n, euler, s, st);
+  xform32_back(c, G, scratch, fhT, fin, out, n, euler, s, st, gs);
   c.prof.end(3, st);
   return cuda_status(cudaPeekAtLastError(), "fast collision");
 }

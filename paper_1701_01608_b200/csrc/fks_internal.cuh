@@ -97,10 +97,19 @@ GenericWs generic_ws(const Ctx& c, long long n);
 void generic_forward(Ctx& c, const double* fin, long long n, cudaStream_t st);
 void generic_back(Ctx& c, const double* fin, double* out, long long n, bool euler, double s, cudaStream_t st);
 
+// Transport fused into the fast path's first and last kernels: the input of cell j (chunk-local index j - cell0)
+// is f*[j][k] = base[(j - delta(k)) mod grid][k], read directly from the untransported f_in.
+struct GatherSrc {
+  const double* base;   // f_in of the whole grid
+  Shift sh;
+  long long cell0;      // global index of the chunk's first cell
+  int in16;             // base 16-byte aligned
+};
+
 // fast path (fast32.cu)
 bool fast_available(const Ctx& c);
 fks_status fast_collision(Ctx& c, const double* fin, double* out, long long n_cells, bool euler, double s,
-                          cudaStream_t st);
+                          cudaStream_t st, const GatherSrc* gs = nullptr);
 size_t fast_ws_bytes_per_cell(const Ctx& c);
 fks_status fast_prepare(Ctx& c);
 

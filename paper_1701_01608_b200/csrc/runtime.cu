@@ -124,8 +124,10 @@ static long long chunk_cells(const Ctx& c, size_t per_cell, long long n_cells) {
 }
 
 // Collision (+ optional Euler) over n cells resident on the device, chunked through the workspace.
+// With `gs` (fast path only) the input is not materialised: cell j's f* is gathered from gs->base by the first
+// and last kernels (transport fused); `fin` is then unused and cells [gs->cell0, +n) are computed.
 static fks_status run_collision(Ctx& c, const double* fin, double* out, long long n, bool euler, double s,
-                                cudaStream_t st) {
+                                cudaStream_t st, const GatherSrc* gs = nullptr) {
   const bool fast = c.path == FKS_PATH_FAST;
   size_t per_cell = fast ? fast_ws_bytes_per_cell(c) : generic_ws_bytes_per_cell(c);
   long long ch = chunk_cells(c, per_cell, n);
@@ -134,11 +136,26 @@ static fks_status run_collision(Ctx& c, const double* fin, double* out, long lon
   const size_t nv = (size_t)c.N * c.N * c.N;
   for (long long c0 = 0; c0 < n; c0 += ch) {
     long long m = std::min(ch, n - c0);
-    rc = fast ? fast_collision(c, fin + c0 * nv, out + c0 * nv, m, euler, s, st)
-              : generic_collision(c, fin + c0 * nv, out + c0 * nv, m, euler, s, st);
+    if (gs) {
+      GatherSrc g = *gs;
+      g.cell0 = gs->cell0 + c0;
+      rc = fast_collision(c, nullptr, out + c0 * nv, m, euler, s, st, &g);
+    } else {
+      rc = fast ? fast_collision(c, fin + c0 * nv, out + c0 * nv, m, euler, s, st)
+                : generic_collision(c, fin + c0 * nv, out + c0 * nv, m, euler, s, st);
+    }
     if (rc) return rc;
   }
   return cuda_status(cudaPeekAtLastError(), "collision launch");
+}
+
+static GatherSrc make_gather(const double* base, const Shift& sh, long long cell0) {
+  GatherSrc g{};
+  g.base = base;
+  g.sh = sh;
+  g.cell0 = cell0;
+  g.in16 = ((uintptr_t)base & 15) == 0;
+  return g;
 }
 
 static Shift advance_generic_cell(Ctx& c) {
@@ -405,6 +422,10 @@ fks_status fks_step(fks_ctx* h, const double* f_in, double* f_out, double coll_s
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   Shift sh = advance_generic_cell(c);
   if (shift_is_identity(sh)) return run_collision(c, f_in, f_out, n, true, coll_scale, st);
+  if (c.path == FKS_PATH_FAST && !std::getenv("FKS_UNFUSED_TRANSPORT")) {  // transport fused into kf1 / kb3
+    const GatherSrc g = make_gather(f_in, sh, 0);
+    return run_collision(c, nullptr, f_out, n, true, coll_scale, st, &g);
+  }
   // transport (exact permutation) into f_out, then collision + Euler in place on f_out
   c.prof.begin(0, st);
   rc = launch_transport_gather(c, f_in, f_out, sh, st);
@@ -527,7 +548,10 @@ fks_status fks_step_host(fks_ctx* h, const double* f_in_host, double* f_out_host
     rc = cuda_status(cudaStreamWaitEvent(st, eh[i], 0), "wait H2D");
     if (!rc) {
       if (ident) rc = run_collision(c, c.d_stage_in + c0 * nv, c.d_stage_out + c0 * nv, m, true, coll_scale, st);
-      else {
+      else if (c.path == FKS_PATH_FAST && !std::getenv("FKS_UNFUSED_TRANSPORT")) {
+        const GatherSrc g = make_gather(c.d_stage_in, sh, c0);
+        rc = run_collision(c, nullptr, c.d_stage_out + c0 * nv, m, true, coll_scale, st, &g);
+      } else {
         rc = launch_transport_gather(c, c.d_stage_in, c.d_stage_out, sh, st, c0, m);
         if (!rc) rc = run_collision(c, c.d_stage_out + c0 * nv, c.d_stage_out + c0 * nv, m, true, coll_scale, st);
       }

@@ -62,15 +62,54 @@ struct InModes32 {  // x[i], i = k mod 32 for k in K' (16 absent); rows stored a
 // ---- forward ------------------------------------------------------------------------------------------
 // kf1: CTA = (cell, 8 jx planes).  z: real FFT32 per row (two reals packed per complex, FFT16, untangle),
 // lz = 0..15;  y: FFT32 over jy -> ly in K'.  Out F2[cell][jx][ly][lz].
-__global__ void __launch_bounds__(256) kf1(const double* __restrict__ f, double2* __restrict__ F2) {
+// Source cells of the fused transport for destination cell j (global) and velocity planes jx0..jx0+7:
+// sx[pl] (x index of plane jx0+pl), sy[jy], sz[jz], as in the transport gather kernel.
+__device__ __forceinline__ void gather_tables(const GatherSrc& g, long long j, int jx0, int* sx, int* sy, int* sz) {
+  const Shift& sh = g.sh;
+  const int jz = (int)(j % sh.nz), jy = (int)((j / sh.nz) % sh.ny), jxc = (int)(j / ((long long)sh.nz * sh.ny));
+  const int k = threadIdx.x;
+  if (k < N) {
+    int b = (jy - sh.delta[1][k]) % sh.ny; if (b < 0) b += sh.ny;
+    int c = (jz - sh.delta[2][k]) % sh.nz; if (c < 0) c += sh.nz;
+    sy[k] = b; sz[k] = c;
+  }
+  if (k < PL8) {
+    int a = (jxc - sh.delta[0][jx0 + k]) % sh.nx; if (a < 0) a += sh.nx;
+    sx[k] = a;
+  }
+}
+
+__global__ void __launch_bounds__(256) kf1(const double* __restrict__ f, double2* __restrict__ F2, const GatherSrc g,
+                                           int gather) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* buf = reinterpret_cast<double2*>(smem_raw);  // [8][32][RS] (rows padded: conflict-free row tasks)
+  __shared__ int sx[PL8], sy[N], sz[N];
   const int tid = threadIdx.x;
   const long long cell = blockIdx.x / (N / PL8);
   const int jx0 = (blockIdx.x % (N / PL8)) * PL8;
-  const double2* src = reinterpret_cast<const double2*>(f + (cell * N + jx0) * N * N);
+  if (!gather) {
+    const double2* src = reinterpret_cast<const double2*>(f + (cell * N + jx0) * N * N);
 #pragma unroll 4
-  for (int i = tid; i < PL8 * N * H; i += 256) cp16(buf + (i >> 4) * RS + (i & 15), src + i);
+    for (int i = tid; i < PL8 * N * H; i += 256) cp16(buf + (i >> 4) * RS + (i & 15), src + i);
+  } else {  // fused transport: pairs (jz, jz+1) from one source cell move as 16 bytes, others as two 8-byte copies
+    gather_tables(g, g.cell0 + cell, jx0, sx, sy, sz);
+    __syncthreads();
+    const long long nv = (long long)N * N * N;
+#pragma unroll 4
+    for (int i = tid; i < PL8 * N * H; i += 256) {
+      const int pl = i >> 9, jy = (i >> 4) & 31, jz = 2 * (i & 15);
+      const long long row = (long long)sx[pl] * g.sh.ny + sy[jy];
+      const long long s0 = row * g.sh.nz + sz[jz], s1 = row * g.sh.nz + sz[jz + 1];
+      const long long off = ((long long)(jx0 + pl) * N + jy) * N + jz;
+      double2* d = buf + (i >> 4) * RS + (i & 15);
+      if (s0 == s1 && g.in16) {
+        cp16(d, g.base + s0 * nv + off);
+      } else {
+        cp8(d, g.base + s0 * nv + off);
+        cp8(reinterpret_cast<double*>(d) + 1, g.base + s1 * nv + off + 1);
+      }
+    }
+  }
   cp_wait_all();
   __syncthreads();
   {  // z: thread = (plane, jy)
@@ -275,8 +314,9 @@ __global__ void __launch_bounds__(192) kb2(const double2* __restrict__ H2, doubl
 // kb3: CTA = (cell, 8 jx planes).  z: inverse FFT32 over kz -> jz;  y: Hermitian -> real inverse FFT32 (packed
 // FFT16); then Q or f* + s Q, transposed through shared memory into coalesced stores.
 __global__ void __launch_bounds__(256) kb3(const double2* __restrict__ E1, const double* fin, double* out,
-                                           int euler, double s) {
+                                           int euler, double s, const GatherSrc g, int gather) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ int sx[PL8], sy[N], sz[N];
   double2* buf = reinterpret_cast<double2*>(smem_raw);  // [8][32 rows][RS]
   const int tid = threadIdx.x;
   const long long cell = blockIdx.x / (N / PL8);
@@ -334,9 +374,19 @@ __global__ void __launch_bounds__(256) kb3(const double2* __restrict__ E1, const
   const long long base = (cell * N + jx0) * N * N;
   constexpr int PER = PL8 * N * N / 256;  // 32 outputs per thread
   double fv[PER];
-  if (euler) {  // all loads of f* in flight at once
+  if (euler && !gather) {  // all loads of f* in flight at once
 #pragma unroll
     for (int k = 0; k < PER; k++) fv[k] = fin[base + tid + 256 * k];
+  } else if (euler) {  // fused transport: f* gathered from the untransported input
+    gather_tables(g, g.cell0 + cell, jx0, sx, sy, sz);
+    __syncthreads();
+    const long long nv = (long long)N * N * N;
+#pragma unroll
+    for (int k = 0; k < PER; k++) {
+      const int i = tid + 256 * k, pl = i >> 10, jy = (i >> 5) & 31, jz = i & 31;
+      const long long src = ((long long)sx[pl] * g.sh.ny + sy[jy]) * g.sh.nz + sz[jz];
+      fv[k] = __ldg(g.base + src * nv + ((long long)(jx0 + pl) * N + jy) * N + jz);
+    }
   }
 #pragma unroll
   for (int k = 0; k < PER; k++) {
@@ -391,21 +441,26 @@ cudaError_t xform32_prepare() {
   return e;
 }
 
-void xform32_forward(Ctx& c, const double* fin, double2* fhT, double2* scratch, long long n, int nb, cudaStream_t st) {
+void xform32_forward(Ctx& c, const double* fin, double2* fhT, double2* scratch, long long n, int nb, cudaStream_t st,
+                     const GatherSrc* gs) {
   using namespace x32;
   const long long ncol = n * K;
-  kf1<<<(unsigned)(n * (N / PL8)), 256, PL8 * N * RS * 16, st>>>(fin, scratch);
+  GatherSrc g{};
+  if (gs) g = *gs;
+  kf1<<<(unsigned)(n * (N / PL8)), 256, PL8 * N * RS * 16, st>>>(fin, scratch, g, gs ? 1 : 0);
   kf2<<<(unsigned)((ncol + PL8 - 1) / PL8), 256, PL8 * N * H * 16, st>>>(scratch, fhT, ncol, nb);
   c.launches += 2;
 }
 
 void xform32_back(Ctx& c, const double* G, double2* scratch_a, double2* scratch_b, const double* fin, double* out,
-                  long long n, bool euler, double s, cudaStream_t st) {
+                  long long n, bool euler, double s, cudaStream_t st, const GatherSrc* gs) {
   using namespace x32;
   const long long ncol = n * K;
+  GatherSrc g{};
+  if (gs) g = *gs;
   kb1<<<(unsigned)(n * (P / PB1)), 288, PB1 * 24 * ZS * 16, st>>>(G, scratch_a);
   kb2<<<(unsigned)((ncol + PB2 - 1) / PB2), 192, PB2 * (P + K) * H * 16, st>>>(scratch_a, scratch_b, ncol, c.p.project_mass);
-  kb3<<<(unsigned)(n * (N / PL8)), 256, PL8 * N * RS * 16, st>>>(scratch_b, fin, out, euler ? 1 : 0, s);
+  kb3<<<(unsigned)(n * (N / PL8)), 256, PL8 * N * RS * 16, st>>>(scratch_b, fin, out, euler ? 1 : 0, s, g, gs ? 1 : 0);
   c.launches += 3;
 }
 
