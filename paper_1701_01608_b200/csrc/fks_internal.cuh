@@ -37,17 +37,15 @@ struct Ctx {
   int path = FKS_PATH_AUTO;             // resolved path
   // device tables: ab[t][l] = (a_t(l), b_t(l)), t = 0..T, l flattened over K'^3
   double2* d_ab = nullptr;
-  double2* d_abT = nullptr;             // fast path: ab[t][iz][ix*K+iy] (pencil-interleaved, coalesced per lz)
-  int fast_cluster = 0;                 // fast path: CTAs per cell (thread-block cluster size)
-  int fast_ncl = 0;                     // fast path: co-resident clusters (persistent grid)
-  double2* d_w1 = nullptr;
-  long long* dbg = nullptr;
+  double2* d_abT = nullptr;             // fast path: tables restricted to lower-half pencils, per-member blocks
+  double2* d_w1 = nullptr;              // fast path: per-team L2-resident ring of z-pass outputs W1
+  unsigned* d_ctr = nullptr;            // fast path: per-team produce / consume counters of the W1 ring
+  int fast_kernel = 0;                  // fast path term-loop kernel (4 = hot_kernel_v4)
+  int fast_variant = 12;                // fast path: CTAs per cell (team size)
+  int fast_nteams = 0;                  // fast path: co-resident teams (cells in flight)
+  long long* dbg = nullptr;             // debug: hot-kernel phase timestamps (env FKS_PHASE_TIMING)
   long long* prog_host = nullptr;       // debug: mapped pinned per-warp progress words (FKS_DEBUG_PROGRESS)
   long long* prog_dev = nullptr;
-  int fast_kernel = 0;                  // fast path term-loop kernel: 2 = 6-CTA clusters, 3 = t12, 4 = v4
-  int fast_variant = 6;                 // fast path: CTAs per cell (6 = cluster kernel, 12 = two-CTAs-per-SM teams)
-  int fast_nteams = 0;                  // fast path (variant 12): co-resident teams
-  unsigned* d_ctr = nullptr;            // fast path (variant 12): team-barrier counters             // debug: hot-kernel phase timestamps (env FKS_PHASE_TIMING)              // fast path: per-cluster double-buffered z-pass exchange (L2-resident)
   std::vector<double> dirs, w;          // host copy of directions / weights
   std::vector<double> kappa;            // exact power-of-two balance per term (device tables hold a*kappa, b/kappa)
   // twiddles e^{+2 pi i m/M} for M = N and M = P

@@ -665,7 +665,7 @@ fks_status fks_get_fast_layout(const fks_ctx* h, int* ctas_per_cell, int* concur
   const Ctx& c = *reinterpret_cast<const Ctx*>(h);
   const bool fast = c.path == FKS_PATH_FAST;
   if (ctas_per_cell) *ctas_per_cell = fast ? c.fast_variant : 0;
-  if (concurrent_cells) *concurrent_cells = fast ? (c.fast_kernel >= 3 ? c.fast_nteams : c.fast_ncl) : 0;
+  if (concurrent_cells) *concurrent_cells = fast ? c.fast_nteams : 0;
   return FKS_OK;
 }
 
