@@ -19,7 +19,9 @@
  *    and asynchronous unless stated.  No exception crosses the ABI.
  *  - Validation errors return before any launch.  Asynchronous kernel faults surface as FKS_ERR_CUDA on the
  *    next call or on fks_sync.  fks_last_error() returns a thread-local message for the last failure.
- *  - A handle is used from one host thread at a time.  Tables are immutable after init.
+ *  - A handle is used from one host thread at a time.  Tables are immutable after init.  Calls on one handle
+ *    are serialised in submission order even across streams: each call's stream first waits for the work the
+ *    previous call on the handle enqueued (an internal event), because they share the handle's workspace.
  *  - Inputs and outputs must not overlap (checked by pointer range): FKS_ERR_INVALID.
  *  - There is no CPU fallback: without a CUDA device every compute call returns FKS_ERR_CUDA.
  */
@@ -70,7 +72,8 @@ typedef struct {
   int pad;                      /* 0 = P = 3N/2 (default, A10); else explicit P in [N, 4N]: P >= 3N/2-2 is
                                    the exact Galerkin operator, P < 3N/2-2 the aliased collocation operator
                                    (pairs with l+m = k mod P; P = N: classical collocation; generic path)   */
-  double cutoff_ratio;          /* Carleman cutoff R_c = ratio*R; 0 or 1 = paper-literal (A7), max 1.7072  */
+  double cutoff_ratio;          /* Carleman cutoff R_c = ratio*R: 0 (default) or in [1, 1.7071] (A7);
+                                   1 = paper-literal; ratios in (0, 1) are rejected (FKS_ERR_INVALID)        */
   int project_mass;             /* 1 = set Q^_0 := 0 exactly (A24); default 0                              */
   long long max_cells_in_flight;/* workspace limit in cells per chunk; 0 = auto                            */
   int path;                     /* fks_path                                                                */
@@ -121,6 +124,9 @@ fks_status fks_transport_setup_slab(fks_ctx* h, int nx_global, int ny, int nz, i
 
 /* Halo width H = an upper bound of max |delta_x| over all steps (ceil(cfl) + 1). */
 fks_status fks_slab_halo(const fks_ctx* h, int* halo);
+
+/* Length nx_local + 2H of the `planes` table the _slab calls read (FKS_ERR_STATE before the slab setup). */
+fks_status fks_slab_plane_count(const fks_ctx* h, int* n_planes);
 
 /* One transport step of the local cells, gathering across the slab boundary directly from the owner's memory:
  * `planes` is a HOST array of nx_local + 2H DEVICE pointers; planes[i] is global x-plane (x0 - H + i) mod

@@ -25,7 +25,8 @@ EXPORTS = ["fks_collision_init", "fks_collision_init_ex", "fks_collision_batch",
            "fks_get_fast_layout",
            "fks_get_tables", "fks_get_last_shift", "fks_profile", "fks_profile_read", "fks_debug_timestamps", "fks_launch_count",
            "fks_sync", "fks_destroy", "fks_last_error", "fks_moments", "fks_bgk_batch", "fks_bgk_step",
-           "fks_transport_setup_slab", "fks_slab_halo", "fks_transport_step_slab", "fks_step_slab"]
+           "fks_transport_setup_slab", "fks_slab_halo", "fks_slab_plane_count", "fks_transport_step_slab",
+           "fks_step_slab"]
 
 
 class fks_params(C.Structure):
@@ -70,6 +71,7 @@ def load_library(path: str = None):
         "fks_moments": ([vp, vp, vp, vp, ll, vp], i),
         "fks_transport_setup_slab": ([vp, i, i, i, i, i, ll, ll], i),
         "fks_slab_halo": ([vp, C.POINTER(i)], i),
+        "fks_slab_plane_count": ([vp, C.POINTER(i)], i),
         "fks_transport_step_slab": ([vp, vp, vp, vp], i),
         "fks_step_slab": ([vp, vp, vp, d, vp], i),
         "fks_bgk_batch": ([vp, vp, vp, d, ll, vp], i),
@@ -174,8 +176,18 @@ def fks_slab_halo(h: int) -> int:
     return H.value
 
 
-def _plane_array(planes):
-    """HOST array of device pointers (ints or tensors) for the _slab calls."""
+def fks_slab_plane_count(h: int) -> int:
+    n = C.c_int()
+    _check(load_library().fks_slab_plane_count(h, C.byref(n)))
+    return n.value
+
+
+def _plane_array(h: int, planes):
+    """HOST array of device pointers (ints or tensors) for the _slab calls; the C side reads exactly
+    fks_slab_plane_count(h) entries, so the length is checked here."""
+    want = fks_slab_plane_count(h)
+    if len(planes) != want:
+        raise FksError(1, f"planes has {len(planes)} entries, the slab needs nx_local + 2*halo = {want}")
     arr = (C.c_void_p * len(planes))()
     for i, p in enumerate(planes):
         arr[i] = _ptr(p)
@@ -183,11 +195,11 @@ def _plane_array(planes):
 
 
 def fks_transport_step_slab(h: int, planes, f_out, stream=None):
-    _check(load_library().fks_transport_step_slab(h, _plane_array(planes), _ptr(f_out), _stream(stream)))
+    _check(load_library().fks_transport_step_slab(h, _plane_array(h, planes), _ptr(f_out), _stream(stream)))
 
 
 def fks_step_slab(h: int, planes, f_out, coll_scale: float, stream=None):
-    _check(load_library().fks_step_slab(h, _plane_array(planes), _ptr(f_out), coll_scale, _stream(stream)))
+    _check(load_library().fks_step_slab(h, _plane_array(h, planes), _ptr(f_out), coll_scale, _stream(stream)))
 
 
 def fks_moments(h: int, f, U=None, W=None, n_cells: int | None = None, stream=None):

@@ -70,6 +70,10 @@ struct Ctx {
   std::vector<long long> offsets;       // [3][N] in units of 1/(N*cfl_den) cell
   Shift last{};
   long long launches = 0;
+  // stream ordering across calls: every call first waits for the previous call's work on this handle (the
+  // workspace, W1 ring and team counters are per handle), whatever stream either ran on
+  cudaEvent_t ev_done = nullptr;
+  bool ev_pending = false;
   PhaseTimer prof;
   int num_sms = 148;
 };

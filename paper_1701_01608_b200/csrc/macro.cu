@@ -85,6 +85,9 @@ __global__ void __launch_bounds__(NT) macro_kernel(const Args A) {
   const int q0 = rank * A.chunk;
   const int q1 = (int)min((long long)q0 + A.chunk, nv);  // this CTA's velocity points are [q0, q1)
   const int nh = max(q1 - q0, 0);
+  // Distributed shared memory may only be accessed once every CTA of the cluster is running: arrive here, wait
+  // just before the DSMEM push below (the wait hides behind the staging copies).
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
 
   // ---- stage the cell's points in shared memory (asynchronous copies, all in flight at once) ----
   if (MODE == BGK_STEP) {  // source cell of every (axis, velocity index): (j - delta) mod grid
@@ -160,6 +163,7 @@ __global__ void __launch_bounds__(NT) macro_kernel(const Args A) {
     for (int a = 0; a < 5; a++) s_red[tid >> 5][a] = m[a];
   }
   __syncthreads();
+  asm volatile("barrier.cluster.wait.aligned;" ::: "memory");  // every peer CTA has started
   if (tid < 5 * A.C) {  // push this CTA's partial sum of component a into CTA r's s_part[rank][a]
     const int a = tid % 5, r = tid / 5;
     double s = 0.0;

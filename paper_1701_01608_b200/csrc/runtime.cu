@@ -112,6 +112,25 @@ static fks_status ensure_ws(Ctx& c, size_t bytes) {
   return FKS_OK;
 }
 
+// Calls on one handle share its device workspace, W1 ring and team counters, so they are serialised in
+// submission order across streams: a call's stream waits for the event recorded by the previous call, and the
+// call records the event on its own stream when its work is enqueued (two streams must not race on
+// one handle's workspace).
+static fks_status order_begin(Ctx& c, cudaStream_t st) {
+  if (!c.ev_done) {
+    cudaError_t e = cudaEventCreateWithFlags(&c.ev_done, cudaEventDisableTiming);
+    if (e != cudaSuccess) { cudaGetLastError(); return cuda_status(e, "ordering event"); }
+  }
+  if (!c.ev_pending) return FKS_OK;
+  return cuda_status(cudaStreamWaitEvent(st, c.ev_done, 0), "stream ordering");
+}
+static fks_status order_end(Ctx& c, cudaStream_t st, fks_status rc) {
+  if (!c.ev_done) return rc;
+  fks_status r2 = cuda_status(cudaEventRecord(c.ev_done, st), "stream ordering");
+  if (r2 == FKS_OK) c.ev_pending = true;
+  return rc ? rc : r2;
+}
+
 static long long chunk_cells(const Ctx& c, size_t per_cell, long long n_cells) {
   long long lim = c.p.max_cells_in_flight;
   if (lim <= 0) {
@@ -218,8 +237,10 @@ fks_status fks_collision_init_ex(fks_ctx** out, const fks_params* pp) {
     return FKS_ERR_INVALID;
   }
   if (p.quad_rule != FKS_QUAD_GL_UNIFORM && p.quad_rule != FKS_QUAD_PAPER_RECT) { set_error("unknown quadrature rule"); return FKS_ERR_UNSUPPORTED; }
-  if (p.cutoff_ratio < 0.0 || p.cutoff_ratio > (1.0 + std::sqrt(2.0)) / std::sqrt(2.0) + 1e-12) {
-    set_error("cutoff_ratio must be in [1, (1+sqrt2)/sqrt2] (A7)"); return FKS_ERR_INVALID;
+  // 0 = default (R_c = R); otherwise R_c/R in [1, (1+sqrt2)/sqrt2]: below 1 the cutoff would truncate the
+  // support of the Carleman integral (A7), above it the periodised collision partners alias
+  if (!(p.cutoff_ratio == 0.0 || (p.cutoff_ratio >= 1.0 && p.cutoff_ratio <= (1.0 + std::sqrt(2.0)) / std::sqrt(2.0) + 1e-12))) {
+    set_error("cutoff_ratio must be 0 (default) or in [1, (1+sqrt2)/sqrt2] (A7)"); return FKS_ERR_INVALID;
   }
   if (p.path < FKS_PATH_AUTO || p.path > FKS_PATH_FAST) { set_error("unknown path"); return FKS_ERR_UNSUPPORTED; }
   int P = p.pad > 0 ? p.pad : 3 * p.N / 2;
@@ -293,7 +314,9 @@ fks_status fks_collision_batch(fks_ctx* h, const double* f, double* Q, long long
   size_t bytes = (size_t)n_cells * c.N * c.N * c.N * sizeof(double);
   if (overlap(f, bytes, Q, bytes)) { set_error("Q overlaps f"); return FKS_ERR_INVALID; }
   if ((rc = sticky_check())) return rc;
-  return run_collision(c, f, Q, n_cells, false, 0.0, reinterpret_cast<cudaStream_t>(stream));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if ((rc = order_begin(c, st))) return rc;
+  return order_end(c, st, run_collision(c, f, Q, n_cells, false, 0.0, st));
 }
 
 fks_status fks_transport_setup(fks_ctx* h, int nx, int ny, int nz, long long cfl_num, long long cfl_den) {
@@ -340,6 +363,14 @@ fks_status fks_slab_halo(const fks_ctx* h, int* halo) {
   return FKS_OK;
 }
 
+fks_status fks_slab_plane_count(const fks_ctx* h, int* n_planes) {
+  if (!h || !n_planes) { set_error("NULL argument"); return FKS_ERR_INVALID; }
+  const Ctx& c = *reinterpret_cast<const Ctx*>(h);
+  if (!c.transport_ready || !c.slab) { set_error("fks_transport_setup_slab not called"); return FKS_ERR_STATE; }
+  *n_planes = c.nx + 2 * c.halo;
+  return FKS_OK;
+}
+
 static fks_status slab_table(Ctx& c, const double* const* planes, double* f_out, PlaneTable& tab) {
   if (!c.transport_ready || !c.slab) { set_error("fks_transport_setup_slab not called"); return FKS_ERR_STATE; }
   if (!planes) { set_error("planes is NULL"); return FKS_ERR_INVALID; }
@@ -350,6 +381,7 @@ static fks_status slab_table(Ctx& c, const double* const* planes, double* f_out,
   const size_t out_bytes = plane_bytes * c.nx;
   for (int i = 0; i < np; i++) {
     if (!planes[i]) { set_error("planes[i] is NULL"); return FKS_ERR_INVALID; }
+    if ((rc = check_device_ptr(planes[i], "planes[i]"))) return rc;  // device or peer-mapped memory
     if (overlap(planes[i], plane_bytes, f_out, out_bytes)) { set_error("a source plane overlaps f_out"); return FKS_ERR_INVALID; }
     tab.p[i] = planes[i];
   }
@@ -363,12 +395,13 @@ fks_status fks_transport_step_slab(fks_ctx* h, const double* const* planes, doub
   fks_status rc;
   if ((rc = slab_table(c, planes, f_out, tab))) return rc;
   if ((rc = sticky_check())) return rc;
-  Shift sh = advance_generic_cell(c);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if ((rc = order_begin(c, st))) return rc;
+  Shift sh = advance_generic_cell(c);
   c.prof.begin(0, st);
   rc = launch_transport_gather_slab(c, tab, f_out, sh, st);
   c.prof.end(0, st);
-  return rc;
+  return order_end(c, st, rc);
 }
 
 fks_status fks_step_slab(fks_ctx* h, const double* const* planes, double* f_out, double coll_scale, void* stream) {
@@ -379,13 +412,14 @@ fks_status fks_step_slab(fks_ctx* h, const double* const* planes, double* f_out,
   fks_status rc;
   if ((rc = slab_table(c, planes, f_out, tab))) return rc;
   if ((rc = sticky_check())) return rc;
-  Shift sh = advance_generic_cell(c);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if ((rc = order_begin(c, st))) return rc;
+  Shift sh = advance_generic_cell(c);
   c.prof.begin(0, st);
   rc = launch_transport_gather_slab(c, tab, f_out, sh, st);
   c.prof.end(0, st);
-  if (rc) return rc;
-  return run_collision(c, f_out, f_out, (long long)c.nx * c.ny * c.nz, true, coll_scale, st);
+  if (!rc) rc = run_collision(c, f_out, f_out, (long long)c.nx * c.ny * c.nz, true, coll_scale, st);
+  return order_end(c, st, rc);
 }
 
 fks_status fks_transport_step(fks_ctx* h, const double* f_in, double* f_out, void* stream) {
@@ -399,12 +433,13 @@ fks_status fks_transport_step(fks_ctx* h, const double* f_in, double* f_out, voi
   size_t bytes = (size_t)n * c.N * c.N * c.N * sizeof(double);
   if (overlap(f_in, bytes, f_out, bytes)) { set_error("f_out overlaps f_in"); return FKS_ERR_INVALID; }
   if ((rc = sticky_check())) return rc;
-  Shift sh = advance_generic_cell(c);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if ((rc = order_begin(c, st))) return rc;
+  Shift sh = advance_generic_cell(c);
   c.prof.begin(0, st);
   rc = launch_transport_gather(c, f_in, f_out, sh, st);
   c.prof.end(0, st);
-  return rc;
+  return order_end(c, st, rc);
 }
 
 fks_status fks_step(fks_ctx* h, const double* f_in, double* f_out, double coll_scale, void* stream) {
@@ -420,18 +455,19 @@ fks_status fks_step(fks_ctx* h, const double* f_in, double* f_out, double coll_s
   if (overlap(f_in, bytes, f_out, bytes)) { set_error("f_out overlaps f_in"); return FKS_ERR_INVALID; }
   if ((rc = sticky_check())) return rc;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if ((rc = order_begin(c, st))) return rc;
   Shift sh = advance_generic_cell(c);
-  if (shift_is_identity(sh)) return run_collision(c, f_in, f_out, n, true, coll_scale, st);
+  if (shift_is_identity(sh)) return order_end(c, st, run_collision(c, f_in, f_out, n, true, coll_scale, st));
   if (c.path == FKS_PATH_FAST && !std::getenv("FKS_UNFUSED_TRANSPORT")) {  // transport fused into kf1 / kb3
     const GatherSrc g = make_gather(f_in, sh, 0);
-    return run_collision(c, nullptr, f_out, n, true, coll_scale, st, &g);
+    return order_end(c, st, run_collision(c, nullptr, f_out, n, true, coll_scale, st, &g));
   }
   // transport (exact permutation) into f_out, then collision + Euler in place on f_out
   c.prof.begin(0, st);
   rc = launch_transport_gather(c, f_in, f_out, sh, st);
   c.prof.end(0, st);
-  if (rc) return rc;
-  return run_collision(c, f_out, f_out, n, true, coll_scale, st);
+  if (!rc) rc = run_collision(c, f_out, f_out, n, true, coll_scale, st);
+  return order_end(c, st, rc);
 }
 
 static fks_status ensure_stage(Ctx& c, long long cells) {
@@ -464,6 +500,7 @@ fks_status fks_collision_batch_host(fks_ctx* h, const double* f_host, double* Q_
   const long long nv = (long long)c.N * c.N * c.N;
   const long long nch = std::max(1LL, std::min(32LL, n_cells / 512));
   cudaStream_t st = c.stage_stream;
+  if ((rc = order_begin(c, st)) || (rc = order_begin(c, c.h2d_stream))) return rc;
   std::vector<cudaEvent_t> eh(nch), ec(nch);
   for (long long i = 0; i < nch; i++) {
     cudaEventCreateWithFlags(&eh[i], cudaEventDisableTiming);
@@ -488,6 +525,7 @@ fks_status fks_collision_batch_host(fks_ctx* h, const double* f_host, double* Q_
   cudaStreamSynchronize(st);
   cudaStreamSynchronize(c.h2d_stream);
   for (long long i = 0; i < nch; i++) { cudaEventDestroy(eh[i]); cudaEventDestroy(ec[i]); }
+  c.ev_pending = false;  // everything this handle enqueued has completed
   return rc ? rc : rs;
 }
 
@@ -511,6 +549,7 @@ fks_status fks_step_host(fks_ctx* h, const double* f_in_host, double* f_out_host
   const long long plane = (long long)c.ny * c.nz;          // cells per x-plane (contiguous)
   const size_t pbytes = (size_t)plane * nv * sizeof(double);
   cudaStream_t st = c.stage_stream;
+  if ((rc = order_begin(c, st)) || (rc = order_begin(c, c.h2d_stream))) return rc;
   const Shift sh = advance_generic_cell(c);
   int dmax = 0;
   for (int k = 0; k < c.N; k++) dmax = std::max(dmax, std::abs(sh.delta[0][k]));
@@ -565,6 +604,7 @@ fks_status fks_step_host(fks_ctx* h, const double* f_in_host, double* f_out_host
   cudaStreamSynchronize(st);
   cudaStreamSynchronize(c.h2d_stream);
   for (int i = 0; i < nch; i++) { cudaEventDestroy(eh[i]); cudaEventDestroy(ec[i]); }
+  c.ev_pending = false;  // everything this handle enqueued has completed
   return rc ? rc : rs;
 }
 
@@ -592,7 +632,9 @@ fks_status fks_moments(fks_ctx* h, const double* f, double* U, double* W, long l
   const size_t bytes = (size_t)n_cells * c.N * c.N * c.N * sizeof(double);
   if ((rc = check_opt_moments(c, U, W, n_cells, f, bytes))) return rc;
   if ((rc = sticky_check())) return rc;
-  return launch_macro(c, 0, f, nullptr, U, W, n_cells, 0.0, nullptr, reinterpret_cast<cudaStream_t>(stream));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if ((rc = order_begin(c, st))) return rc;
+  return order_end(c, st, launch_macro(c, 0, f, nullptr, U, W, n_cells, 0.0, nullptr, st));
 }
 
 fks_status fks_bgk_batch(fks_ctx* h, const double* f, double* Q, double nu, long long n_cells, void* stream) {
@@ -606,7 +648,9 @@ fks_status fks_bgk_batch(fks_ctx* h, const double* f, double* Q, double nu, long
   const size_t bytes = (size_t)n_cells * c.N * c.N * c.N * sizeof(double);
   if (overlap(f, bytes, Q, bytes)) { set_error("Q overlaps f"); return FKS_ERR_INVALID; }
   if ((rc = sticky_check())) return rc;
-  return launch_macro(c, 1, f, Q, nullptr, nullptr, n_cells, nu, nullptr, reinterpret_cast<cudaStream_t>(stream));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if ((rc = order_begin(c, st))) return rc;
+  return order_end(c, st, launch_macro(c, 1, f, Q, nullptr, nullptr, n_cells, nu, nullptr, st));
 }
 
 fks_status fks_bgk_step(fks_ctx* h, const double* f_in, double* f_out, double nu_dt, double* U, double* W,
@@ -627,8 +671,10 @@ fks_status fks_bgk_step(fks_ctx* h, const double* f_in, double* f_out, double nu
     return FKS_ERR_INVALID;
   }
   if ((rc = sticky_check())) return rc;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if ((rc = order_begin(c, st))) return rc;
   Shift sh = advance_generic_cell(c);
-  return launch_macro(c, 2, f_in, f_out, U, W, n, nu_dt, &sh, reinterpret_cast<cudaStream_t>(stream));
+  return order_end(c, st, launch_macro(c, 2, f_in, f_out, U, W, n, nu_dt, &sh, st));
 }
 
 fks_status fks_get_info(const fks_ctx* h, int* P, int* T, double* R, double* lambda) {
@@ -746,6 +792,7 @@ void fks_destroy(fks_ctx* h) {
   if (c->stage_stream) cudaStreamDestroy(c->stage_stream);
   if (c->h2d_stream) cudaStreamDestroy(c->h2d_stream);
   if (c->d2h_stream) cudaStreamDestroy(c->d2h_stream);
+  if (c->ev_done) cudaEventDestroy(c->ev_done);
   for (int ph = 0; ph < 4; ph++)
     for (auto& ev : c->prof.used[ph]) c->prof.pool.push_back(ev);
   for (auto& ev : c->prof.pool) { cudaEventDestroy(ev.first); cudaEventDestroy(ev.second); }

@@ -64,6 +64,22 @@ def test_argument_validation_without_gpu(lib):
     assert lib.fks_step(None, None, None, 0.1, None) == binding.FKS_ERR_INVALID
 
 
+def test_cutoff_ratio_range_without_gpu(lib):
+    """R_c / R below 1 would truncate the Carleman integral (A7): rejected before any device work; 0 is the
+    default sentinel and [1, (1+sqrt2)/sqrt2] is accepted (FKS_ERR_CUDA here only because there is no GPU)."""
+    import torch
+
+    def init(ratio):
+        p = binding.fks_params(N=16, L=13.24, M_angles=16, M_radial=16, kernel=0, cutoff_ratio=ratio)
+        h = ctypes.c_void_p()
+        return lib.fks_collision_init_ex(ctypes.byref(h), ctypes.byref(p))
+    for bad in (0.5, 0.999, -1.0, 1.8):
+        assert init(bad) == binding.FKS_ERR_INVALID, bad
+    if not torch.cuda.is_available():
+        for good in (0.0, 1.0, 1.5):
+            assert init(good) == binding.FKS_ERR_CUDA, good
+
+
 def test_product_never_imports_oracle():
     pkg = os.path.join(ROOT, "paper_1701_01608_b200")
     for dirpath, _, files in os.walk(pkg):
