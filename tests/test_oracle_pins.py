@@ -63,6 +63,26 @@ def test_P2_paper_rule():
         assert abs(np.sum(w) - (math.pi ** 2 / nt) / math.tan(math.pi / (2 * nt))) < 1e-12
 
 
+@pytest.mark.parametrize("nt,nf", [(4, 4), (8, 4), (8, 8), (16, 2)])
+def test_P2_paper_rule_second_moments(nt, nf):
+    """The paper's rectangle rule (θ_p = pπ/n_θ, φ_q = qπ/n_φ, w = π²/(n_θ n_φ) sin θ_p)
+    pinned beyond Σw by closed forms of its second moments.  With Σ_{p<n} sin(mπp/n) = cot(mπ/2n) for odd m and
+    sin θ cos²θ = (sin θ + sin 3θ)/4, sin³θ = (3 sin θ − sin 3θ)/4, Σ_q cos²φ_q = n_φ/2 (n_φ ≥ 2):
+      Σ w e_z² = (π²/4n_θ)[cot(π/2n_θ) + cot(3π/2n_θ)],
+      Σ w e_x² = Σ w e_y² = (π²/8n_θ)[3 cot(π/2n_θ) − cot(3π/2n_θ)],  off-diagonals 0;
+    both tend to the continuum 2π/3 (a wrong node set, weight or sin θ placement breaks the identities)."""
+    e, w = o.directions(nt, nf, o.QUAD_PAPER_RECT)
+    c1, c3 = 1 / math.tan(math.pi / (2 * nt)), 1 / math.tan(3 * math.pi / (2 * nt))
+    m = np.einsum("d,da,db->ab", w, e, e)
+    zz = math.pi ** 2 / (4 * nt) * (c1 + c3)
+    xx = math.pi ** 2 / (8 * nt) * (3 * c1 - c3)
+    assert abs(m[2, 2] - zz) < 1e-12 and abs(m[0, 0] - xx) < 1e-12 and abs(m[1, 1] - xx) < 1e-12
+    assert np.abs(m - np.diag(np.diag(m))).max() < 1e-12
+    # second-order convergence of the rectangle rule to the continuum value 2π/3
+    z2 = math.pi ** 2 / (8 * nt) * (1 / math.tan(math.pi / (4 * nt)) + 1 / math.tan(3 * math.pi / (4 * nt)))
+    assert 3.5 < abs(zz - 2 * math.pi / 3) / abs(z2 - 2 * math.pi / 3) < 4.5
+
+
 # ---------------- P3 φ_R and ψ_R against quadrature of their defining integrals ----------------------
 
 @pytest.mark.parametrize("s", [0.0, 0.05, 0.3, 1.7, 3.9, 6.6])
@@ -351,6 +371,43 @@ def test_P15_transport_permutation():
         src = o.source_cells(j, shape, d1)
         ref = np.take_along_axis(f.reshape(n, -1), src.reshape(1, -1), 0).reshape(N, N, N)
         assert np.array_equal(o.transport(f, shape, d1)[j], ref)
+
+
+def test_P15_single_particle_moves_with_its_velocity():
+    """External pin of the shift DIRECTION (the exact solution of the free transport is
+    f(t + dt, x) = f(t, x - v dt), i.e. a particle at x moves to x + v dt).  One particle in cell (0, 0, 0)
+    with velocity v = (L/2, 0, -L/2) (node indices 3N/4, N/2, N/4 of v_k = -L + 2Lk/N, A13) and CFL c = 2
+    (dt = 2 dx/L): v dt = (+1, 0, -1) cells, so after one step it must sit in cell (1, 0, nz - 1) and nowhere
+    else; after n steps in (n mod nx, 0, -n mod nz).  With c = 1 it advances one cell every second step."""
+    N, shape = 8, (5, 3, 4)
+    nx, ny, nz = shape
+    k = (3 * N // 4, N // 2, N // 4)
+    v = -L + 2 * L * np.array(k) / N
+    assert np.allclose(v, (L / 2, 0.0, -L / 2))
+    f = np.zeros((nx * ny * nz, N, N, N))
+    f[0][k] = 1.0
+    cell = o.GenericCell(N=N, c_num=2, c_den=1)
+    cur = f
+    for n in range(1, 7):
+        cur = o.transport(cur, shape, cell.advance())
+        where = np.argwhere(cur[:, k[0], k[1], k[2]] == 1.0).ravel()
+        assert where.tolist() == [((n % nx) * ny + 0) * nz + (-n) % nz], (n, where)
+        assert cur.sum() == 1.0
+    # half a cell per step (c = 1): x advances by one cell every second step, the v = 0 axis never moves
+    cell = o.GenericCell(N=N, c_num=1, c_den=1)
+    cur = f
+    xs = []
+    for n in range(1, 9):
+        cur = o.transport(cur, shape, cell.advance())
+        j = int(np.argwhere(cur[:, k[0], k[1], k[2]] == 1.0).ravel()[0])
+        xs.append((j // (ny * nz), (j // nz) % ny))
+    assert [x for x, _ in xs] == [(n + 1) // 2 % nx for n in range(1, 9)] and all(y == 0 for _, y in xs)
+    # a particle with negative velocity moves the other way
+    g = np.zeros_like(f)
+    g[0][N // 4, N // 2, N // 2] = 1.0   # v = (-L/2, 0, 0)
+    cell = o.GenericCell(N=N, c_num=2, c_den=1)
+    g = o.transport(g, shape, cell.advance())
+    assert np.argwhere(g[:, N // 4, N // 2, N // 2] == 1.0).ravel().tolist() == [((nx - 1) * ny) * nz]
 
 
 # ---------------- P16: Euler ---------------------------------------------------------------------------
