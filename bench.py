@@ -106,6 +106,13 @@ class ClockSampler:
 # ------------------------------------------------------------------------------------------------------
 
 def oracle_threads() -> int:
+    """Host threads the C++ oracle's std::thread pool uses (every core this process may run on)."""
+    from oracle import cpp_oracle as co
+    return co.default_threads()
+
+
+def blas_threads() -> int:
+    """Threads the numpy (BLAS) oracle may use: the BGK leg still times the numpy oracle."""
     try:
         from threadpoolctl import threadpool_info
         n = [i.get("num_threads", 1) for i in threadpool_info() if i.get("user_api") == "blas"]
@@ -114,24 +121,41 @@ def oracle_threads() -> int:
         return os.cpu_count() or 1
 
 
-def time_oracle(cfg, budget_s: float, max_cells: int = 256) -> dict:
-    """Oracle fks_step on sampled cells of the workload (transport is a permutation of inputs; collision +
-    Euler per sampled cell), until `budget_s` of CPU time has elapsed."""
-    import numpy as np
-    from oracle import fks_oracle as o
+def host_cpu() -> dict:
+    """nproc and CPU model of the host the oracle is timed on."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "affinity": oracle_threads(), "model": model}
+
+
+def time_oracle(cfg, budget_s: float, max_cells: int = 256, min_batches: int = 1) -> dict:
+    """The plain C++17 oracle (oracle/cpp, std::thread pool over cells, naive per-axis DFTs; BJ.north_star) on
+    sampled cells of the workload: collision + Euler per sampled cell (the transport is a permutation of the
+    inputs), one batch of `threads` cells at a time, until `budget_s` has elapsed."""
+    from oracle import cpp_oracle as co
     from paper_1701_01608_b200 import inputs
-    tb = o.build_tables(cfg.N, cfg.L, M=cfg.M, M_r=cfg.M_r, kernel=cfg.kernel)
+    tb = co.build_tables(cfg.N, cfg.L, M=cfg.M, M_r=cfg.M_r, kernel=cfg.kernel)
+    thr = co.default_threads()
     cells = inputs.sample_cells(cfg, min(max_cells, cfg.n_cells), seed=5)
     f = inputs.make_f(cfg, cells=cells).numpy()
     t0 = time.perf_counter()
-    n = 0
-    for fc in f:
-        o.euler(fc, o.collision_fast(fc, tb), cfg.coll_scale)
-        n += 1
-        if time.perf_counter() - t0 > budget_s:
+    n = nb = 0
+    while n < len(f):
+        batch = f[n:n + thr]
+        co.euler(batch, co.collision_batch(batch, tb, threads=thr), cfg.coll_scale)
+        n += len(batch)
+        nb += 1
+        if nb >= min_batches and time.perf_counter() - t0 > budget_s:
             break
     dt = time.perf_counter() - t0
-    return {"cells": n, "seconds": dt, "value": n * cfg.N ** 3 / dt}
+    return {"cells": n, "seconds": dt, "value": n * cfg.N ** 3 / dt, "threads": thr}
 
 
 # ------------------------------------------------------------------------------------------------------
@@ -203,7 +227,7 @@ def run_bgk(args):
                           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
                           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
                           "data": "synthetic", "config": workload,
-                          "cpu_baseline": {"value": val, "unit": unit, "cores": oracle_threads(), "kind": "oracle",
+                          "cpu_baseline": {"value": val, "unit": unit, "cores": blas_threads(), "kind": "oracle",
                                            "sample": f"{cells} cells of {cfg.name} (BGK relaxation per sampled cell)"},
                           "e2e": {"value": val, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
         return
@@ -285,7 +309,7 @@ def run_bgk(args):
                      "kernel": "macro_kernel<BGK_STEP> (fused transport gather + moments + relaxation)",
                      "bytes_per_cell_vp": 16, "peak_note": peak_note},
         "clocks": clk.summary(), "gpu_launches": launches, "e2e": e2e,
-        "cpu_baseline": {"value": cpu["value"], "unit": unit, "cores": oracle_threads(), "kind": "oracle",
+        "cpu_baseline": {"value": cpu["value"], "unit": unit, "cores": blas_threads(), "kind": "oracle",
                          "sample": f"{cpu['cells']} sampled cells of {cfg.name}, BGK relaxation, {cpu['seconds']:.1f} s"},
     }))
     if ws > 1:
@@ -331,7 +355,7 @@ def main():
         cells = 0
         per_step = max(2.0, min(args.cpu_seconds, 120.0 / max(1, args.steps + args.warmup)))
         for i in range(args.warmup + args.steps):
-            r = time_oracle(cfg, per_step, max_cells=8)
+            r = time_oracle(cfg, per_step, max_cells=oracle_threads())
             if i >= args.warmup:
                 times.append(r["seconds"])
                 cells += r["cells"]
@@ -341,8 +365,10 @@ def main():
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic", "config": workload,
                 "cpu_baseline": {"value": val, "unit": unit, "cores": oracle_threads(), "kind": "oracle",
-                                 "sample": f"{cells} cells of {cfg.name} (collision+Euler per sampled cell), "
-                                           f"{args.steps} steps of ~{per_step:.0f} s"},
+                                 "host": host_cpu(),
+                                 "sample": f"{cells} cells of {cfg.name} (collision+Euler per sampled cell, C++ "
+                                           f"oracle, one batch of {oracle_threads()} cells per step), "
+                                           f"{args.steps} steps"},
                 "e2e": {"value": val, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line))
         return
@@ -484,9 +510,11 @@ def main():
         "path": {1: "generic", 2: "fast"}.get(col.info.get("path"), None),
         "fast_layout": {"ctas_per_cell": col.info.get("ctas_per_cell"), "concurrent_cells": col.info.get("concurrent_cells")},
         "clocks": clocks, "gpu_launches": launches, "e2e": e2e,
-        "cpu_baseline": {"value": cpu["value"], "unit": unit, "cores": oracle_threads(), "kind": "oracle",
+        "cpu_baseline": {"value": cpu["value"], "unit": unit, "cores": cpu["threads"], "kind": "oracle",
+                         "host": host_cpu(),
                          "sample": f"{cpu['cells']} sampled cells of {cfg.name}, collision+Euler, "
-                                   f"{cpu['seconds']:.1f} s (numpy fp64 oracle, naive DFT matrices)"},
+                                   f"{cpu['seconds']:.1f} s (plain C++17 fp64 oracle, naive per-axis DFTs, "
+                                   f"std::thread pool of {cpu['threads']} over cells)"},
     }
     print(json.dumps(line))
     if ws > 1:
