@@ -535,7 +535,7 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
 
 }  // namespace f32
 
-bool fast_available(const Ctx& c) { return c.N == 32 && c.P == 48; }
+bool fast_available(const Ctx& c) { return (c.N == 32 && c.P == 48) || small_available(c); }
 
 size_t xform32_ws_bytes_per_cell();
 cudaError_t xform32_prepare();
@@ -545,9 +545,12 @@ void xform32_forward(Ctx& c, const double* fin, double2* fhT, double2* scratch, 
 void xform32_back(Ctx& c, const double* G, double2* scratch_a, double2* scratch_b, const double* fin, double* out,
                   long long n, bool euler, double s, cudaStream_t st, const GatherSrc* gs);
 
-size_t fast_ws_bytes_per_cell(const Ctx&) { return xform32_ws_bytes_per_cell(); }
+size_t fast_ws_bytes_per_cell(const Ctx& c) {
+  return c.N == 32 ? xform32_ws_bytes_per_cell() : small_ws_bytes_per_cell(c);
+}
 
 fks_status fast_prepare(Ctx& c) {
+  if (c.N != 32) return small_prepare(c);
   using namespace f32;
   cudaError_t e = xform32_prepare();
   if (e == cudaSuccess) e = fftd::fill_twiddles();
@@ -575,6 +578,7 @@ fks_status fast_prepare(Ctx& c) {
 
 fks_status fast_collision(Ctx& c, const double* fin, double* out, long long n, bool euler, double s,
                           cudaStream_t st, const GatherSrc* gs) {
+  if (c.N != 32) return small_collision(c, fin, out, n, euler, s, st, gs);
   using namespace f32;
   // workspace: f^T [n][K^3] complex | scratch [n][P*K*16] complex | G [n][P^3] fp64
   double2* fhT = reinterpret_cast<double2*>(c.d_ws);

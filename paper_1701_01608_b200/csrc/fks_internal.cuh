@@ -76,6 +76,7 @@ struct Ctx {
   bool ev_pending = false;
   PhaseTimer prof;
   int num_sms = 148;
+  int small_ctas = 0;                   // small-N fast path (N = 16, 24): persistent CTAs (SMs x CTAs per SM)
 };
 
 // error plumbing
@@ -114,6 +115,14 @@ fks_status fast_collision(Ctx& c, const double* fin, double* out, long long n_ce
                           cudaStream_t st, const GatherSrc* gs = nullptr);
 size_t fast_ws_bytes_per_cell(const Ctx& c);
 fks_status fast_prepare(Ctx& c);
+
+// small-N fast path (small.cu): N = 16 / 24 with P = 3N/2; generic forward / back transforms around one
+// persistent term-loop kernel (one CTA per (cell, z-class, term chunk) unit)
+bool small_available(const Ctx& c);
+size_t small_ws_bytes_per_cell(const Ctx& c);
+fks_status small_prepare(Ctx& c);
+fks_status small_collision(Ctx& c, const double* fin, double* out, long long n_cells, bool euler, double s,
+                           cudaStream_t st, const GatherSrc* gs);
 
 // transport gather (transport.cu)
 fks_status launch_transport_gather(Ctx& c, const double* fin, double* fout, const Shift& sh, cudaStream_t st,
