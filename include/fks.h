@@ -109,6 +109,16 @@ fks_status fks_transport_step(fks_ctx* h, const double* f_in, double* f_out, voi
  * Euler: f_out = f* + coll_scale * Q(f*), f* = transported f_in, coll_scale = dt/Kn. */
 fks_status fks_step(fks_ctx* h, const double* f_in, double* f_out, double coll_scale, void* stream);
 
+/* fks_step plus the macroscopic moments of the new state (the paper's per-step moment update, Eq. DM_update
+ * P:464-493): U[c] = sum_k phi(v_k) f_out[c][k] dv^3, phi = (1, v, |v|^2/2), and
+ * W[c] = (rho, u, T), exactly as fks_moments defines them, for every cell c of f_out.  U and W are DEVICE arrays
+ * [nx*ny*nz][5] fp64; either may be NULL, not both (FKS_ERR_INVALID); they must not overlap f_in, f_out or each
+ * other.  On the N = 32 fast path the sums are reduced inside the step's last kernel (a fixed-order per-CTA
+ * reduction, then one tiny kernel per chunk), otherwise by one moments pass over f_out.  f_out is bit-identical
+ * to fks_step's; U, W agree with fks_moments(f_out) to rounding (different summation order). */
+fks_status fks_step_moments(fks_ctx* h, const double* f_in, double* f_out, double coll_scale, double* U, double* W,
+                            void* stream);
+
 /* Host-buffer variant of fks_step (synchronous), for the end-to-end measurement.  The step is pipelined over
  * x-slabs (one plane each, up to 32; env FKS_HOST_SLABS overrides) on three streams: copy-in (wrap-around halo
  * first), transport + collision of each slab as soon as its source planes have landed, copy-out.  Pinned host

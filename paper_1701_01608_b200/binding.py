@@ -26,7 +26,7 @@ EXPORTS = ["fks_collision_init", "fks_collision_init_ex", "fks_collision_batch",
            "fks_get_tables", "fks_get_last_shift", "fks_profile", "fks_profile_read", "fks_debug_timestamps", "fks_launch_count",
            "fks_sync", "fks_destroy", "fks_last_error", "fks_moments", "fks_bgk_batch", "fks_bgk_step",
            "fks_transport_setup_slab", "fks_slab_halo", "fks_slab_plane_count", "fks_transport_step_slab",
-           "fks_step_slab"]
+           "fks_step_slab", "fks_step_moments"]
 
 
 class fks_params(C.Structure):
@@ -69,6 +69,7 @@ def load_library(path: str = None):
         "fks_step": ([vp, vp, vp, d, vp], i),
         "fks_step_host": ([vp, vp, vp, d], i),
         "fks_moments": ([vp, vp, vp, vp, ll, vp], i),
+        "fks_step_moments": ([vp, vp, vp, d, vp, vp, vp], i),
         "fks_transport_setup_slab": ([vp, i, i, i, i, i, ll, ll], i),
         "fks_slab_halo": ([vp, C.POINTER(i)], i),
         "fks_slab_plane_count": ([vp, C.POINTER(i)], i),
@@ -159,6 +160,10 @@ def fks_transport_step(h: int, f_in, f_out, stream=None):
 
 def fks_step(h: int, f_in, f_out, coll_scale: float, stream=None):
     _check(load_library().fks_step(h, _ptr(f_in), _ptr(f_out), coll_scale, _stream(stream)))
+
+
+def fks_step_moments(h: int, f_in, f_out, coll_scale: float, U=None, W=None, stream=None):
+    _check(load_library().fks_step_moments(h, _ptr(f_in), _ptr(f_out), coll_scale, _ptr(U), _ptr(W), _stream(stream)))
 
 
 def fks_step_host(h: int, f_in_host, f_out_host, coll_scale: float):
@@ -312,6 +317,14 @@ class Collision:
 
     def step(self, f_in, f_out, coll_scale: float, stream=None):
         fks_step(self.h, f_in, f_out, coll_scale, stream)
+
+    def step_moments(self, f_in, f_out, coll_scale: float, stream=None):
+        """fks_step plus the moments (U, W) of f_out, [n_cells][5] each (fused into the step's last kernel)."""
+        import torch
+        U = torch.empty((f_out.shape[0], 5), dtype=torch.float64, device=f_out.device)
+        W = torch.empty_like(U)
+        fks_step_moments(self.h, f_in, f_out, coll_scale, U, W, stream)
+        return U, W
 
     def moments(self, f, stream=None):
         """(U, W): conservative (ρ, ρu, E) and primitive (ρ, u, T) moments per cell, [n_cells][5] each."""

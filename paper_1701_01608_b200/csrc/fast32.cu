@@ -543,7 +543,7 @@ void xform32_tables_lh(const double2* ab, double2* abL, int T1, int nb);
 void xform32_forward(Ctx& c, const double* fin, double2* fhT, double2* scratch, long long n, int nb, cudaStream_t st,
                      const GatherSrc* gs);
 void xform32_back(Ctx& c, const double* G, double2* scratch_a, double2* scratch_b, const double* fin, double* out,
-                  long long n, bool euler, double s, cudaStream_t st, const GatherSrc* gs);
+                  long long n, bool euler, double s, cudaStream_t st, const GatherSrc* gs, double* mpart);
 
 size_t fast_ws_bytes_per_cell(const Ctx& c) {
   return c.N == 32 ? xform32_ws_bytes_per_cell() : small_ws_bytes_per_cell(c);
@@ -577,8 +577,12 @@ fks_status fast_prepare(Ctx& c) {
 }
 
 fks_status fast_collision(Ctx& c, const double* fin, double* out, long long n, bool euler, double s,
-                          cudaStream_t st, const GatherSrc* gs) {
-  if (c.N != 32) return small_collision(c, fin, out, n, euler, s, st, gs);
+                          cudaStream_t st, const GatherSrc* gs, double* U, double* W) {
+  if (c.N != 32) {
+    fks_status rc = small_collision(c, fin, out, n, euler, s, st, gs);
+    if (!rc && (U || W)) rc = launch_macro(c, 0, out, nullptr, U, W, n, 0.0, nullptr, st);  // separate moments pass
+    return rc;
+  }
   using namespace f32;
   // workspace: f^T [n][K^3] complex | scratch [n][P*K*16] complex | G [n][P^3] fp64
   double2* fhT = reinterpret_cast<double2*>(c.d_ws);
@@ -605,7 +609,21 @@ fks_status fast_collision(Ctx& c, const double* fin, double* out, long long n, b
   if (rc) return rc;
 
   c.prof.begin(3, st);
-  xform32_back(c, G, scratch, fhT, fin, out, n, euler, s, st, gs);
+  double* mpart = nullptr;
+  if (U || W) {  // moments of the step's output, reduced in kb3's epilogue (N / 8 partials per cell)
+    const size_t need = (size_t)n * (N / 8) * 5;
+    if (need > c.mpart_elems) {
+      if (c.d_mpart) cudaFree(c.d_mpart);
+      c.d_mpart = nullptr;
+      c.mpart_elems = 0;
+      cudaError_t e = cudaMalloc(&c.d_mpart, need * sizeof(double));
+      if (e != cudaSuccess) { cudaGetLastError(); c.prof.end(3, st); return cuda_status(e, "moment partials"); }
+      c.mpart_elems = need;
+    }
+    mpart = c.d_mpart;
+  }
+  xform32_back(c, G, scratch, fhT, fin, out, n, euler, s, st, gs, mpart);
+  if (mpart) launch_moments_finish(c, mpart, N / 8, n, U, W, st);
   c.prof.end(3, st);
   return cuda_status(cudaPeekAtLastError(), "fast collision");
 }

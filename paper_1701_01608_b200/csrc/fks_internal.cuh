@@ -77,6 +77,8 @@ struct Ctx {
   PhaseTimer prof;
   int num_sms = 148;
   int small_ctas = 0;                   // small-N fast path (N = 16, 24): persistent CTAs (SMs x CTAs per SM)
+  double* d_mpart = nullptr;            // fks_step_moments: per-CTA partial moment sums of the last kernel
+  size_t mpart_elems = 0;
 };
 
 // error plumbing
@@ -111,8 +113,9 @@ struct GatherSrc {
 
 // fast path (fast32.cu)
 bool fast_available(const Ctx& c);
+// U, W (optional, [n_cells][5]): moments of `out` (NEXT-1), fused into the last kernel on the N = 32 path
 fks_status fast_collision(Ctx& c, const double* fin, double* out, long long n_cells, bool euler, double s,
-                          cudaStream_t st, const GatherSrc* gs = nullptr);
+                          cudaStream_t st, const GatherSrc* gs = nullptr, double* U = nullptr, double* W = nullptr);
 size_t fast_ws_bytes_per_cell(const Ctx& c);
 fks_status fast_prepare(Ctx& c);
 
@@ -140,5 +143,8 @@ fks_status launch_transport_gather_slab(Ctx& c, const PlaneTable& tab, double* f
 // out = f* + coef (E[f*] - f*).  U, W optional ([n_cells][5]).
 fks_status launch_macro(Ctx& c, int mode, const double* fin, double* out, double* U, double* W, long long n_cells,
                         double coef, const Shift* sh, cudaStream_t st);
+// U, W of n_cells cells from per-cell partial sums mpart[cell][parts][5] (summed in order, times dv^3)
+void launch_moments_finish(Ctx& c, const double* mpart, int parts, long long n_cells, double* U, double* W,
+                           cudaStream_t st);
 
 }  // namespace fks

@@ -255,6 +255,39 @@ static cudaError_t launch(const Args& A, size_t smem, cudaStream_t st) {
 }  // namespace macro
 
 // Launch one macro kernel over n_cells cells (MODE: 0 moments, 1 BGK operator, 2 BGK step with transport).
+// U = dv^3 sum_p mpart[cell][p] (p in order), W = (rho, u, T) exactly as macro_kernel derives them
+__global__ void moments_finish_kernel(const double* __restrict__ mpart, int parts, long long n, double h3, double* U,
+                                      double* W) {
+  const long long cell = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (cell >= n) return;
+  double u[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  for (int p = 0; p < parts; p++) {
+#pragma unroll
+    for (int a = 0; a < 5; a++) u[a] += mpart[(cell * parts + p) * 5 + a];
+  }
+#pragma unroll
+  for (int a = 0; a < 5; a++) u[a] *= h3;
+  if (U) {
+#pragma unroll
+    for (int a = 0; a < 5; a++) U[cell * 5 + a] = u[a];
+  }
+  if (W) {
+    const double rho = u[0];
+    const double ux = u[1] / rho, uy = u[2] / rho, uz = u[3] / rho;
+    const double T = (u[4] - 0.5 * rho * (ux * ux + uy * uy + uz * uz)) / (1.5 * rho);
+    double* w = W + cell * 5;
+    w[0] = rho; w[1] = ux; w[2] = uy; w[3] = uz; w[4] = T;
+  }
+}
+
+void launch_moments_finish(Ctx& c, const double* mpart, int parts, long long n_cells, double* U, double* W,
+                           cudaStream_t st) {
+  if (n_cells <= 0) return;
+  const double h = 2.0 * c.p.L / c.N;
+  moments_finish_kernel<<<(unsigned)((n_cells + 127) / 128), 128, 0, st>>>(mpart, parts, n_cells, h * h * h, U, W);
+  c.launches++;
+}
+
 fks_status launch_macro(Ctx& c, int mode, const double* fin, double* out, double* U, double* W, long long n_cells,
                         double coef, const Shift* sh, cudaStream_t st) {
   if (n_cells <= 0) return FKS_OK;

@@ -146,7 +146,7 @@ static long long chunk_cells(const Ctx& c, size_t per_cell, long long n_cells) {
 // With `gs` (fast path only) the input is not materialised: cell j's f* is gathered from gs->base by the first
 // and last kernels (transport fused); `fin` is then unused and cells [gs->cell0, +n) are computed.
 static fks_status run_collision(Ctx& c, const double* fin, double* out, long long n, bool euler, double s,
-                                cudaStream_t st, const GatherSrc* gs = nullptr) {
+                                cudaStream_t st, const GatherSrc* gs = nullptr, double* U = nullptr, double* W = nullptr) {
   const bool fast = c.path == FKS_PATH_FAST;
   size_t per_cell = fast ? fast_ws_bytes_per_cell(c) : generic_ws_bytes_per_cell(c);
   long long ch = chunk_cells(c, per_cell, n);
@@ -155,13 +155,17 @@ static fks_status run_collision(Ctx& c, const double* fin, double* out, long lon
   const size_t nv = (size_t)c.N * c.N * c.N;
   for (long long c0 = 0; c0 < n; c0 += ch) {
     long long m = std::min(ch, n - c0);
+    double* Uc = U ? U + 5 * c0 : nullptr;
+    double* Wc = W ? W + 5 * c0 : nullptr;
     if (gs) {
       GatherSrc g = *gs;
       g.cell0 = gs->cell0 + c0;
-      rc = fast_collision(c, nullptr, out + c0 * nv, m, euler, s, st, &g);
+      rc = fast_collision(c, nullptr, out + c0 * nv, m, euler, s, st, &g, Uc, Wc);
+    } else if (fast) {
+      rc = fast_collision(c, fin + c0 * nv, out + c0 * nv, m, euler, s, st, nullptr, Uc, Wc);
     } else {
-      rc = fast ? fast_collision(c, fin + c0 * nv, out + c0 * nv, m, euler, s, st)
-                : generic_collision(c, fin + c0 * nv, out + c0 * nv, m, euler, s, st);
+      rc = generic_collision(c, fin + c0 * nv, out + c0 * nv, m, euler, s, st);
+      if (!rc && (U || W)) rc = launch_macro(c, 0, out + c0 * nv, nullptr, Uc, Wc, m, 0.0, nullptr, st);
     }
     if (rc) return rc;
   }
@@ -442,7 +446,9 @@ fks_status fks_transport_step(fks_ctx* h, const double* f_in, double* f_out, voi
   return order_end(c, st, rc);
 }
 
-fks_status fks_step(fks_ctx* h, const double* f_in, double* f_out, double coll_scale, void* stream) {
+// fks_step and fks_step_moments: transport, collision + Euler, optional moments of f_out (U, W may be NULL)
+static fks_status step_impl(fks_ctx* h, const double* f_in, double* f_out, double coll_scale, double* U, double* W,
+                            void* stream) {
   if (!h) { set_error("NULL handle"); return FKS_ERR_INVALID; }
   Ctx& c = *reinterpret_cast<Ctx*>(h);
   if (!c.transport_ready) { set_error("fks_transport_setup not called"); return FKS_ERR_STATE; }
@@ -453,21 +459,39 @@ fks_status fks_step(fks_ctx* h, const double* f_in, double* f_out, double coll_s
   long long n = (long long)c.nx * c.ny * c.nz;
   size_t bytes = (size_t)n * c.N * c.N * c.N * sizeof(double);
   if (overlap(f_in, bytes, f_out, bytes)) { set_error("f_out overlaps f_in"); return FKS_ERR_INVALID; }
+  if (U || W) {
+    const size_t mb = (size_t)n * 5 * sizeof(double);
+    if ((U && (rc = check_device_ptr(U, "U"))) || (W && (rc = check_device_ptr(W, "W")))) return rc;
+    if ((U && (overlap(U, mb, f_in, bytes) || overlap(U, mb, f_out, bytes))) ||
+        (W && (overlap(W, mb, f_in, bytes) || overlap(W, mb, f_out, bytes))) || (U && W && overlap(U, mb, W, mb))) {
+      set_error("U / W overlap f_in, f_out or each other"); return FKS_ERR_INVALID;
+    }
+  }
   if ((rc = sticky_check())) return rc;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if ((rc = order_begin(c, st))) return rc;
   Shift sh = advance_generic_cell(c);
-  if (shift_is_identity(sh)) return order_end(c, st, run_collision(c, f_in, f_out, n, true, coll_scale, st));
+  if (shift_is_identity(sh)) return order_end(c, st, run_collision(c, f_in, f_out, n, true, coll_scale, st, nullptr, U, W));
   if (c.path == FKS_PATH_FAST && !std::getenv("FKS_UNFUSED_TRANSPORT")) {  // transport fused into kf1 / kb3
     const GatherSrc g = make_gather(f_in, sh, 0);
-    return order_end(c, st, run_collision(c, nullptr, f_out, n, true, coll_scale, st, &g));
+    return order_end(c, st, run_collision(c, nullptr, f_out, n, true, coll_scale, st, &g, U, W));
   }
   // transport (exact permutation) into f_out, then collision + Euler in place on f_out
   c.prof.begin(0, st);
   rc = launch_transport_gather(c, f_in, f_out, sh, st);
   c.prof.end(0, st);
-  if (!rc) rc = run_collision(c, f_out, f_out, n, true, coll_scale, st);
+  if (!rc) rc = run_collision(c, f_out, f_out, n, true, coll_scale, st, nullptr, U, W);
   return order_end(c, st, rc);
+}
+
+fks_status fks_step(fks_ctx* h, const double* f_in, double* f_out, double coll_scale, void* stream) {
+  return step_impl(h, f_in, f_out, coll_scale, nullptr, nullptr, stream);
+}
+
+fks_status fks_step_moments(fks_ctx* h, const double* f_in, double* f_out, double coll_scale, double* U, double* W,
+                            void* stream) {
+  if (!U && !W) { set_error("fks_step_moments: U and W are both NULL"); return FKS_ERR_INVALID; }
+  return step_impl(h, f_in, f_out, coll_scale, U, W, stream);
 }
 
 static fks_status ensure_stage(Ctx& c, long long cells) {
@@ -781,6 +805,7 @@ void fks_destroy(fks_ctx* h) {
   if (c->d_ab) cudaFree(c->d_ab);
   if (c->d_abT) cudaFree(c->d_abT);
   if (c->d_w1) cudaFree(c->d_w1);
+  if (c->d_mpart) cudaFree(c->d_mpart);
   if (c->dbg) cudaFree(c->dbg);
   if (c->prog_host) cudaFreeHost(c->prog_host);
   if (c->d_ctr) cudaFree(c->d_ctr);

@@ -30,18 +30,18 @@ struct Geo {
   static constexpr int H = N / 2, P = 3 * H, K = N - 1, h = H - 1, KK = K * K, NLOW = (KK + 1) / 2;
   static constexpr int R = H / 4;                         // H = 4 R: FFT_H = radix-R x radix-4
   static constexpr int NZS = (NLOW + 31) / 32;            // Z slots (lower-half pencil + mirror per lane)
-  static constexpr int NYL = K * H, NYS = (NYL + 31) / 32;       // Y lane tasks (lx, q) per class r'
-  static constexpr int NXL = 3 * H * H, NXS = (NXL + 31) / 32;   // X lane tasks (q'', q, rx) per class r'
+  static constexpr int NYL = K * H, NYS = (NYL + 31) / 32;       // Y lane tasks (q, lx) per class r'
+  static constexpr int XSR = (H * H + 31) / 32, NXS = 3 * XSR;  // X slots per x-class rx, per y-class r'
   static constexpr int XQB = (NXS + 3) / 4;               // X TMEM column blocks per class r' and lane quarter
   static constexpr int TCOLS = (3 * XQB * 32 <= 128) ? 128 : (3 * XQB * 32 <= 256 ? 256 : 512);
-  static constexpr int W1_E = KK * H;                     // W1[lx][q][ly]
+  static constexpr int W1_E = KK * H;                     // W1[q][lx][ly]
   static constexpr int W2_E = H * H * K;                  // W2[q''][q][lx]
-  static constexpr int SMEM = (W1_E + 2 * W2_E + P) * 16;
+  static constexpr int SMEM = (W1_E + 2 * W2_E) * 16;
 };
 
 constexpr int kMaxWarps = 12, kMaxItems = 12;
 enum { T_Z = 0, T_Y = 1, T_X = 2 };
-// phases: 0 = A (Z + X of class 2), 1 = B (Y of class 0), 2 = C (X0 + Y1), 3 = D (X1 + Y2)
+// phases: 0 = A (Z + X of class 2), 1 = B (Y0), 2 = C (X0 + Y1), 3 = D (X1 + Y2)
 struct Sched {
   unsigned char cnt[4][kMaxWarps];
   unsigned char item[4][kMaxWarps][kMaxItems];  // (type << 5) | slot
@@ -51,10 +51,10 @@ __constant__ Sched c_sched16, c_sched24;
 struct Args {
   const double2* fhT;   // [cell][K][NLOW]: f^ of the lower-half pencils, lz-major (coalesced over pencils)
   const double2* tabT;  // [t][K][NLOW]: balanced (a_t k_t, b_t / k_t), same layout
-  const double2* twP;   // e^{+2 pi i m/P}, m < P
   double* Gout;         // [cell][S][P^3] (S > 1) or [cell][P^3] (S = 1), layout [px][py][pz]
   long long n_cells;
   int T1, S;            // terms, term chunks per (cell, r)
+  long long* dbg;       // optional clock64 stamps [cta][warp][step] of the first unit (FKS_PHASE_TIMING); nullptr
 };
 
 // ---- small complex helpers ---------------------------------------------------------------------------------
@@ -116,24 +116,31 @@ __device__ __forceinline__ void fft_h(double2 (&u)[4 * R]) {
   for (int q1 = 0; q1 < R; q1++) bfly4(u[4 * q1], u[4 * q1 + 1], u[4 * q1 + 2], u[4 * q1 + 3]);
 }
 
-// class-r combine of one pruned input vector x(l), l = -h..h stored at in(l + h):  u[0] = x(0);
-// u[n] = w_P^{n r} (x(n) + x(n - H) w3^{-r}) for n >= 1.  (c3r, c3i) = w3^{-r}, tw(n) = w_P^{n r}.
-template <int H, class In, class Tw>
-__device__ __forceinline__ void combine(const In& in, int r, double c3r, double c3i, const Tw& tw, double2 (&u)[H]) {
+// twiddles w_P^m = e^{+2 pi i m/P} (P = 24, 36) in the constant bank: indexed by compile-time constants after
+// unrolling, they become constant-bank operands of the DFMA / DMUL instructions (no load instructions)
+__constant__ double2 c_tw24[24], c_tw36[36];
+template <int P>
+__device__ __forceinline__ double2 twc(int m) { return P == 24 ? c_tw24[m % 24] : c_tw36[m % 36]; }
+
+// class-r combine (r a compile-time constant) of one pruned input vector x(l), l = -h..h stored at in(l + h):
+// u[0] = x(0);  u[n] = w_P^{n r} (x(n) + x(n - H) w3^{-r}) for n >= 1,  w3^{-1} = (-1/2, -s3), w3^{-2} = (-1/2, s3)
+template <int H, int r, class In>
+__device__ __forceinline__ void combine(const In& in, double2 (&u)[H]) {
+  constexpr double s3 = 0.86602540378443864676;
+  constexpr double c3i = (r == 1) ? -s3 : s3;
   u[0] = in(H - 1);
-  if (r == 0) {
 #pragma unroll
-    for (int n = 1; n < H; n++) u[n] = cadd(in(n + H - 1), in(n - 1));
-  } else {
-#pragma unroll
-    for (int n = 1; n < H; n++) {
-      const double2 a = in(n + H - 1), v = in(n - 1);
+  for (int n = 1; n < H; n++) {
+    const double2 a = in(n + H - 1), v = in(n - 1);
+    if (r == 0) {
+      u[n] = cadd(a, v);
+    } else {
       double2 acc;
-      acc.x = fma(c3r, v.x, a.x);
+      acc.x = fma(-0.5, v.x, a.x);
       acc.x = fma(-c3i, v.y, acc.x);
-      acc.y = fma(c3r, v.y, a.y);
+      acc.y = fma(-0.5, v.y, a.y);
       acc.y = fma(c3i, v.x, acc.y);
-      u[n] = cmul(tw(n), acc);
+      u[n] = cmul(twc<3 * H>(r * n), acc);
     }
   }
 }
@@ -161,14 +168,123 @@ __device__ __forceinline__ void tmem_st32(uint32_t addr, const uint32_t (&v)[32]
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
 
+
+// ---- the three task kinds (one lane = one class task; the class is a compile-time constant) ----------------------
+// Z: lower-half pencil jj (and its mirror) of class r: products from L2, z-pass, W1[q][lx][ly]
+template <int N, int r>
+__device__ __forceinline__ void z_task(double2* W1, const double2* fh, const double2* tabT, int slot, int lane, int t) {
+  using G = Geo<N>;
+  constexpr int H = G::H, K = G::K, R = G::R, NLOW = G::NLOW;
+  const int j = 32 * slot + lane;
+  const bool act = j < NLOW;
+  const int jj = act ? j : NLOW - 1;
+  const double2* tb = tabT + (long long)t * (K * NLOW) + jj;
+  const double2* fp = fh + jj;
+  // pencil (lx, ly) = lower-half pencil jj, mirror (-lx, -ly):  Zp(lz) = ab(l) f(l),  Zm(lz) = ab(l') conj f(l') with
+  // l' = (lx, ly, -lz) (a_t, b_t even in l; f^ Hermitian).  Stored index i = lz + h.  The inputs are loaded in the
+  // quadruples lz = +-n, +-(H - n) that complete u[n] and u[H - n] of both vectors (few live registers).
+  constexpr double s3 = 0.86602540378443864676;
+  constexpr double c3i = (r == 1) ? -s3 : s3;
+  double2 up[H], um[H];
+  auto prod = [&](int i, double2& zp, double2& zm) {
+    const double2 a = __ldg(tb + (long long)i * NLOW), f = __ldg(fp + (long long)i * NLOW);
+    const double by = a.y * f.y, bx = a.y * f.x;
+    zp = make_double2(fma(a.x, f.x, -by), fma(a.x, f.y, bx));   // ab * f
+    zm = make_double2(fma(a.x, f.x, by), fma(-a.x, f.y, bx));   // ab * conj f
+  };
+  auto comb = [&](double2 a, double2 v, int n) {  // w_P^{n r} (a + v w3^{-r})
+    if (r == 0) return cadd(a, v);
+    double2 acc;
+    acc.x = fma(-0.5, v.x, a.x);
+    acc.x = fma(-c3i, v.y, acc.x);
+    acc.y = fma(-0.5, v.y, a.y);
+    acc.y = fma(c3i, v.x, acc.y);
+    return cmul(twc<3 * H>(r * n), acc);
+  };
+  prod(H - 1, up[0], um[0]);  // lz = 0
+#pragma unroll
+  for (int n = 1; n <= H / 2; n++) {
+    // lz = n (idx n+h) -> A, -n (h-n) -> B, n-H (n-1) -> C, H-n (K-n) -> D
+    double2 pA, mA, pB, mB, pC, mC, pD, mD;
+    prod(n + H - 1, pA, mA);
+    prod(n - 1, pC, mC);
+    if (n < H / 2) {
+      prod(H - 1 - n, pB, mB);
+      prod(K - n, pD, mD);
+    } else {
+      pB = pC; mB = mC; pD = pA; mD = mA;
+    }
+    // pencil: x(n) = pA, x(n-H) = pC, x(H-n) = pD, x(-n) = pB;  mirror: x(n) = mB, x(n-H) = mD, x(H-n) = mC, x(-n) = mA
+    up[n] = comb(pA, pC, n);
+    um[n] = comb(mB, mD, n);
+    if (n < H / 2) {
+      up[H - n] = comb(pD, pB, H - n);
+      um[H - n] = comb(mC, mA, H - n);
+    }
+  }
+  const int ix = jj / K, iy = jj - ix * K;
+  fft_h<R>(up);
+  if (act) {
+#pragma unroll
+    for (int q = 0; q < H; q++) W1[(q * K + ix) * K + iy] = up[qslot<R>(q)];
+  }
+  fft_h<R>(um);
+  if (act && j != NLOW - 1) {  // the centre pencil (0, 0) is its own mirror
+#pragma unroll
+    for (int q = 0; q < H; q++) W1[(q * K + (K - 1 - ix)) * K + (K - 1 - iy)] = um[qslot<R>(q)];
+  }
+}
+
+// Y: lane task tau = q K + lx of y-class rp: W1[q][lx][.] along ly -> W2[q''][q][lx]
+template <int N, int rp>
+__device__ __forceinline__ void y_task(const double2* W1, double2* W2b, int slot, int lane) {
+  using G = Geo<N>;
+  constexpr int H = G::H, K = G::K, R = G::R;
+  const int tau = 32 * slot + lane;
+  const bool act = tau < G::NYL;
+  const int tt = act ? tau : G::NYL - 1;
+  const double2* in = W1 + tt * K;
+  double2 u[H];
+  combine<H, rp>([&](int i) { return in[i]; }, u);
+  fft_h<R>(u);
+  if (act) {
+    const int q = tt / K, ix = tt - q * K;
+    double2* out = W2b + q * K + ix;
+#pragma unroll
+    for (int q2 = 0; q2 < H; q2++) out[q2 * H * K] = u[qslot<R>(q2)];
+  }
+}
+
+// X: slot of x-class rx (uniform per slot, lane task pen = q'' H + q): W2[q''][q][.] along lx -> G += Re z Im z
+template <int N, int rx>
+__device__ __forceinline__ void x_task(const double2* W2b, uint32_t col, int pen) {
+  using G = Geo<N>;
+  constexpr int H = G::H, K = G::K, R = G::R;
+  const bool act = pen < H * H;
+  const double2* in = W2b + (act ? pen : H * H - 1) * K;
+  double2 u[H];
+  combine<H, rx>([&](int i) { return in[i]; }, u);
+  fft_h<R>(u);
+  uint32_t gw[32];
+  tmem_ld32(col, gw);
+#pragma unroll
+  for (int q = 0; q < H; q++) {
+    const double2 z = u[qslot<R>(q)];
+    const double g = __hiloint2double((int)gw[2 * q + 1], (int)gw[2 * q]);
+    const double acc = act ? fma(z.x, z.y, g) : g;
+    gw[2 * q] = (uint32_t)__double2loint(acc);
+    gw[2 * q + 1] = (uint32_t)__double2hiint(acc);
+  }
+  tmem_st32(col, gw);  // (an asynchronous load issued before the transform measured 3 % slower on c1)
+}
+
 template <int N, int WARPS>
 __global__ void __launch_bounds__(32 * WARPS, N == 16 ? 2 : 1) small_term_kernel(Args A) {
   using G = Geo<N>;
-  constexpr int H = G::H, P = G::P, K = G::K, R = G::R, NLOW = G::NLOW;
+  constexpr int H = G::H, P = G::P, K = G::K, NLOW = G::NLOW;
   extern __shared__ __align__(16) unsigned char smem[];
   double2* W1 = reinterpret_cast<double2*>(smem);
   double2* W2 = W1 + G::W1_E;              // [2][H][H][K]
-  double2* tws = W2 + 2 * G::W2_E;         // [P]
   __shared__ uint32_t tmem_base_sh;
   const Sched& sc = (N == 16) ? c_sched16 : c_sched24;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -177,7 +293,6 @@ __global__ void __launch_bounds__(32 * WARPS, N == 16 ? 2 : 1) small_term_kernel
                  ::"r"((uint32_t)__cvta_generic_to_shared(&tmem_base_sh)), "r"(G::TCOLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  for (int m = tid; m < P; m += 32 * WARPS) tws[m] = A.twP[m];
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -191,8 +306,6 @@ __global__ void __launch_bounds__(32 * WARPS, N == 16 ? 2 : 1) small_term_kernel
     const long long cell = u / (3 * A.S);
     const int r = (int)((u / A.S) % 3), ch = (int)(u % A.S);
     const int t0 = (int)((long long)ch * A.T1 / A.S), t1 = (int)((long long)(ch + 1) * A.T1 / A.S);
-    // w3^{-r} for the unit's z-class
-    const double c3r = -0.5, c3i = (r == 1) ? -0.86602540378443864676 : 0.86602540378443864676;
     // zero this warp's G blocks (the X blocks it runs in phases A / C / D)
     {
       uint32_t zw[32];
@@ -211,147 +324,55 @@ __global__ void __launch_bounds__(32 * WARPS, N == 16 ? 2 : 1) small_term_kernel
     }
     const double2* fh = A.fhT + cell * (long long)(K * NLOW);
 
-    auto z_task = [&](int slot, int t) {
-      const int j = 32 * slot + lane;
-      const bool act = j < NLOW;
-      const int jj = act ? j : NLOW - 1;
-      const double2* tb = A.tabT + (long long)t * (K * NLOW) + jj;
-      const double2* fp = fh + jj;
-      // pencil (lx, ly) = lower-half pencil jj, mirror (-lx, -ly):  Zp(lz) = ab(l) f(l),  Zm(lz) = ab(l') conj f(l')
-      // with l' = (lx, ly, -lz) (a_t, b_t even in l; f^ Hermitian).  Inputs indexed by lz + h.
-      double2 up[H], um[H];
-      auto prod = [&](int i, double2& zp, double2& zm) {  // index i = lz + h of the stored pencil
-        const double2 a = __ldg(tb + (long long)i * NLOW), f = __ldg(fp + (long long)i * NLOW);
-        const double by = a.y * f.y, bx = a.y * f.x;
-        zp = make_double2(fma(a.x, f.x, -by), fma(a.x, f.y, bx));   // ab * f
-        zm = make_double2(fma(a.x, f.x, by), fma(-a.x, f.y, bx));   // ab * conj f
-      };
-      {
-        double2 p0, m0;
-        prod(H - 1, p0, m0);  // lz = 0
-        up[0] = p0;
-        um[0] = m0;
-      }
-#pragma unroll
-      for (int n = 1; n <= H / 2; n++) {
-        // lz = n (idx n+h), -n (h-n), n-H (n-1), H-n (K-n)
-        double2 pA, mA, pB, mB, pC, mC, pD, mD;
-        prod(n + H - 1, pA, mA);
-        prod(n - 1, pC, mC);
-        if (n < H / 2) {
-          prod(H - 1 - n, pB, mB);
-          prod(K - n, pD, mD);
-        } else {
-          pB = pC; mB = mC; pD = pA; mD = mA;
-        }
-        // pencil:  x(n) = pA, x(n-H) = pC;  x(H-n) = pD, x(-n) = pB
-        // mirror:  x(n) = mB, x(n-H) = mD;  x(H-n) = mC, x(-n) = mA
-        auto comb = [&](double2 a, double2 v, int nn) {
-          if (r == 0) return cadd(a, v);
-          double2 acc;
-          acc.x = fma(c3r, v.x, a.x);
-          acc.x = fma(-c3i, v.y, acc.x);
-          acc.y = fma(c3r, v.y, a.y);
-          acc.y = fma(c3i, v.x, acc.y);
-          return cmul(tws[(r * nn) % P], acc);
-        };
-        up[n] = comb(pA, pC, n);
-        um[n] = comb(mB, mD, n);
-        if (n < H / 2) {
-          up[H - n] = comb(pD, pB, H - n);
-          um[H - n] = comb(mC, mA, H - n);
-        }
-      }
-      const int ix = jj / K, iy = jj - ix * K;
-      fft_h<R>(up);
-      if (act) {
-#pragma unroll
-        for (int q = 0; q < H; q++) W1[(ix * H + q) * K + iy] = up[qslot<R>(q)];
-      }
-      fft_h<R>(um);
-      if (act && j != NLOW - 1) {  // the centre pencil (0, 0) is its own mirror
-#pragma unroll
-        for (int q = 0; q < H; q++) W1[((K - 1 - ix) * H + q) * K + (K - 1 - iy)] = um[qslot<R>(q)];
-      }
-    };
-
-    auto y_task = [&](int slot, int rp, int b) {
-      const int tau = 32 * slot + lane;
-      const bool act = tau < G::NYL;
-      const int tt = act ? tau : G::NYL - 1;
-      const int ix = tt / H, q = tt - ix * H;
-      const double2* in = W1 + (ix * H + q) * K;
-      const double d3i = (rp == 1) ? -0.86602540378443864676 : 0.86602540378443864676;
-      double2 uu[H];
-      combine<H>([&](int i) { return in[i]; }, rp, -0.5, d3i, [&](int n) { return tws[(rp * n) % P]; }, uu);
-      fft_h<R>(uu);
-      if (act) {
-        double2* out = W2 + b * G::W2_E + q * K + ix;
-#pragma unroll
-        for (int q2 = 0; q2 < H; q2++) out[q2 * H * K] = uu[qslot<R>(q2)];
-      }
-    };
-
-    auto x_task = [&](int slot, int rp, int b) {
-      const int tau = 32 * slot + lane;
-      const bool act = tau < G::NXL;
-      const int tt = act ? tau : G::NXL - 1;
-      const int pen = tt / 3, rx = tt - 3 * pen;  // pen = q'' H + q
-      const double2* in = W2 + b * G::W2_E + pen * K;
-      // per-lane class rx (branch-free): w3^{-rx} = (1, 0) for rx = 0, (-1/2, -+sin(2 pi/3)) otherwise
-      const double e3r = rx ? -0.5 : 1.0;
-      const double e3i = rx == 0 ? 0.0 : (rx == 1 ? -0.86602540378443864676 : 0.86602540378443864676);
-      double2 uu[H];
-      uu[0] = in[H - 1];
-#pragma unroll
-      for (int n = 1; n < H; n++) {
-        const double2 a = in[n + H - 1], v = in[n - 1];
-        double2 acc;
-        acc.x = fma(e3r, v.x, a.x);
-        acc.x = fma(-e3i, v.y, acc.x);
-        acc.y = fma(e3r, v.y, a.y);
-        acc.y = fma(e3i, v.x, acc.y);
-        uu[n] = cmul(tws[rx * n], acc);
-      }
-      fft_h<R>(uu);
-      uint32_t gw[32];
-      const uint32_t col = xcol(rp, slot);
-      tmem_ld32(col, gw);
-#pragma unroll
-      for (int q = 0; q < H; q++) {
-        const double2 z = uu[qslot<R>(q)];
-        const double g = __hiloint2double((int)gw[2 * q + 1], (int)gw[2 * q]);
-        const double acc = act ? fma(z.x, z.y, g) : g;
-        gw[2 * q] = (uint32_t)__double2loint(acc);
-        gw[2 * q + 1] = (uint32_t)__double2hiint(acc);
-      }
-      tmem_st32(col, gw);
-    };
-
+    int dstep = 0;
     // phase runner: X items of class xr (-1: skip X), Z items of term zt (-1: skip Z), Y items of class yr
     auto run_phase = [&](int ph, int zt, int xr, int xb, int yr, int yb) {
 #pragma unroll 1
       for (int i = 0; i < sc.cnt[ph][warp]; i++) {
         const int it = sc.item[ph][warp][i];
         const int ty = it >> 5, s = it & 31;
-        if (ty == T_Z) { if (zt >= 0) z_task(s, zt); }
-        else if (ty == T_Y) y_task(s, yr, yb);
-        else if (xr >= 0) x_task(s, xr, xb);
+        if (ty == T_Z) {
+          if (zt >= 0) {
+            if (r == 0) z_task<N, 0>(W1, fh, A.tabT, s, lane, zt);
+            else if (r == 1) z_task<N, 1>(W1, fh, A.tabT, s, lane, zt);
+            else z_task<N, 2>(W1, fh, A.tabT, s, lane, zt);
+          }
+        } else if (ty == T_Y) {
+          if (yr < 0) continue;
+          double2* W2b = W2 + yb * G::W2_E;
+          if (yr == 0) y_task<N, 0>(W1, W2b, s, lane);
+          else if (yr == 1) y_task<N, 1>(W1, W2b, s, lane);
+          else y_task<N, 2>(W1, W2b, s, lane);
+        } else if (xr >= 0) {
+          const double2* W2b = W2 + xb * G::W2_E;
+          const int rx = s / G::XSR, pen = 32 * (s - rx * G::XSR) + lane;
+          const uint32_t col = xcol(xr, s);
+          if (rx == 0) x_task<N, 0>(W2b, col, pen);
+          else if (rx == 1) x_task<N, 1>(W2b, col, pen);
+          else x_task<N, 2>(W2b, col, pen);
+        }
       }
+      if (A.dbg && u == blockIdx.x && blockIdx.x < 32 && lane == 0 && dstep < 64) A.dbg[((long long)blockIdx.x * 16 + warp) * 128 + 2 * dstep] = clock64();
       __syncthreads();
+      if (A.dbg && u == blockIdx.x && blockIdx.x < 32 && lane == 0 && dstep < 64) A.dbg[((long long)blockIdx.x * 16 + warp) * 128 + 2 * dstep + 1] = clock64();
+      dstep++;
     };
 
-    int wb = 0;  // W2 buffer of the next Y pass
+    // phase sequence (ONE call site of run_phase keeps one copy of every task body in the kernel):
+    //   per term t:  A: Z(t) + X2(t-1) [X2 reads the buffer Y2(t-1) wrote]   B: Y0(t) -> wb
+    //                C: X0(t) from wb, Y1(t) -> wb^1    D: X1(t) from wb^1, Y2(t) -> wb    (then wb ^= 1)
+    //   and a final drain phase A with X2(t1 - 1) only.  (Moving X2(t-1) into B, next to Y0(t), measured 4 %
+    //   slower: phase A then holds only the long Z tasks.)
+    int wb = 0;  // W2 buffer of the next Y0 pass
+    const int nsteps = 4 * (t1 - t0) + 1;
 #pragma unroll 1
-    for (int t = t0; t < t1; t++) {
-      // A: Z(t) + X2(t-1) (its Y2 wrote buffer wb ^ 1)
-      run_phase(0, t, t > t0 ? 2 : -1, wb ^ 1, 0, 0);
-      run_phase(1, -1, -1, 0, 0, wb);          // B: Y0(t) -> wb
-      run_phase(2, -1, 0, wb, 1, wb ^ 1);      // C: X0(t) from wb, Y1(t) -> wb^1
-      run_phase(3, -1, 1, wb ^ 1, 2, wb);      // D: X1(t) from wb^1, Y2(t) -> wb
-      wb ^= 1;
+    for (int k = 0; k < nsteps; k++) {
+      const int ph = k & 3, t = t0 + (k >> 2);
+      if (ph == 0) run_phase(0, t < t1 ? t : -1, t > t0 ? 2 : -1, wb ^ 1, -1, 0);
+      else if (ph == 1) run_phase(1, -1, -1, 0, 0, wb);
+      else if (ph == 2) run_phase(2, -1, 0, wb, 1, wb ^ 1);
+      else { run_phase(3, -1, 1, wb ^ 1, 2, wb); wb ^= 1; }
     }
-    run_phase(0, -1, 2, wb ^ 1, 0, 0);         // drain: X2(t1 - 1)
 
     // write the unit's G block: G[px = 3q' + rx][py = 3q'' + r'][pz = 3q + r]
     double* Gc = A.Gout + (A.S > 1 ? (cell * A.S + ch) : cell) * (long long)(P * P * P);
@@ -366,9 +387,8 @@ __global__ void __launch_bounds__(32 * WARPS, N == 16 ? 2 : 1) small_term_kernel
         const int s = it & 31;
         uint32_t gw[32];
         tmem_ld32(xcol(rp, s), gw);
-        const int tau = 32 * s + lane;
-        if (tau < G::NXL) {
-          const int pen = tau / 3, rx = tau - 3 * pen;
+        const int rx = s / G::XSR, pen = 32 * (s - rx * G::XSR) + lane;
+        if (pen < H * H) {
           const int q2 = pen / H, q = pen - q2 * H;
           const int py = 3 * q2 + rp, pz = 3 * q + r;
 #pragma unroll
@@ -463,6 +483,15 @@ static fks_status small_prepare_n(Ctx& c) {
   constexpr int W = sm::warps_for<N>();
   sm::Sched s = sm::make_schedule<N>(W);
   cudaError_t e = cudaMemcpyToSymbol(N == 16 ? sm::c_sched16 : sm::c_sched24, &s, sizeof(s));
+  {  // w_P^m, long double accuracy
+    double2 tw[G::P];
+    const long double pi = 3.14159265358979323846264338327950288L;
+    for (int m = 0; m < G::P; m++) tw[m] = make_double2((double)cosl(2.0L * pi * m / G::P), (double)sinl(2.0L * pi * m / G::P));
+    if (e == cudaSuccess) {
+      if constexpr (N == 16) e = cudaMemcpyToSymbol(sm::c_tw24, tw, sizeof(tw));
+      else e = cudaMemcpyToSymbol(sm::c_tw36, tw, sizeof(tw));
+    }
+  }
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(sm::small_term_kernel<N, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
   int per_sm = 0;
@@ -522,7 +551,7 @@ static fks_status small_collision_n(Ctx& c, const double* fin, double* out, long
 
   c.prof.begin(2, st);
   const int S = small_chunks(c);
-  sm::Args A{fhT, c.d_abT, c.d_twP, S > 1 ? Gp : w.G, n, c.T + 1, S};
+  sm::Args A{fhT, c.d_abT, S > 1 ? Gp : w.G, n, c.T + 1, S, c.dbg};
   const long long units = 3 * n * S;
   const unsigned grid = (unsigned)std::min<long long>(units, c.small_ctas);
   sm::small_term_kernel<N, W><<<grid, 32 * W, G::SMEM, st>>>(A);

@@ -314,7 +314,8 @@ __global__ void __launch_bounds__(192) kb2(const double2* __restrict__ H2, doubl
 // kb3: CTA = (cell, 8 jx planes).  z: inverse FFT32 over kz -> jz;  y: Hermitian -> real inverse FFT32 (packed
 // FFT16); then Q or f* + s Q, transposed through shared memory into coalesced stores.
 __global__ void __launch_bounds__(256) kb3(const double2* __restrict__ E1, const double* fin, double* out,
-                                           int euler, double s, const GatherSrc g, int gather) {
+                                           int euler, double s, const GatherSrc g, int gather, double* mpart,
+                                           double L, double hv) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ int sx[PL8], sy[N], sz[N];
   double2* buf = reinterpret_cast<double2*>(smem_raw);  // [8][32 rows][RS]
@@ -388,12 +389,46 @@ __global__ void __launch_bounds__(256) kb3(const double2* __restrict__ E1, const
       fv[k] = __ldg(g.base + src * nv + ((long long)(jx0 + pl) * N + jy) * N + jz);
     }
   }
+  // moments of the written values (NEXT-1, Eq. DM_update): this CTA's partial sums of
+  // phi(v) f over its 8 planes, phi = (1, v, |v|^2/2), in a fixed order (thread, warp butterfly, warps in order)
+  double m[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  const double vz = __dadd_rn(-L, __dmul_rn((double)(tid & 31), hv));  // v_k = -L + k h, as fks_moments
+  const double wz = 0.5 * vz * vz;
 #pragma unroll
   for (int k = 0; k < PER; k++) {
     const int i = tid + 256 * k, pl = i >> 10, jy = (i >> 5) & 31, jz = i & 31;
     double v = stg[(pl * N + jy) * OS + jz];
     if (euler) v = fma(s, v, fv[k]);
     out[base + i] = v;
+    if (mpart) {
+      const double vx = __dadd_rn(-L, __dmul_rn((double)(jx0 + pl), hv));
+      const double vy = __dadd_rn(-L, __dmul_rn((double)jy, hv));
+      m[0] += v;
+      m[1] = fma(v, vx, m[1]);
+      m[2] = fma(v, vy, m[2]);
+      m[3] = fma(v, vz, m[3]);
+      m[4] = fma(v, 0.5 * vx * vx + 0.5 * vy * vy + wz, m[4]);
+    }
+  }
+  if (mpart) {
+#pragma unroll
+    for (int a = 0; a < 5; a++) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) m[a] += __shfl_xor_sync(0xffffffffu, m[a], o);
+    }
+    __syncthreads();  // the staging region is free: reuse it for the per-warp partials
+    double* red = reinterpret_cast<double*>(smem_raw);
+    if ((tid & 31) == 0) {
+#pragma unroll
+      for (int a = 0; a < 5; a++) red[(tid >> 5) * 5 + a] = m[a];
+    }
+    __syncthreads();
+    if (tid < 5) {
+      double acc = 0.0;
+#pragma unroll
+      for (int w = 0; w < 8; w++) acc += red[w * 5 + tid];
+      mpart[blockIdx.x * 5LL + tid] = acc;  // [cell][N / PL8 plane groups][5]
+    }
   }
 }
 
@@ -453,14 +488,15 @@ void xform32_forward(Ctx& c, const double* fin, double2* fhT, double2* scratch, 
 }
 
 void xform32_back(Ctx& c, const double* G, double2* scratch_a, double2* scratch_b, const double* fin, double* out,
-                  long long n, bool euler, double s, cudaStream_t st, const GatherSrc* gs) {
+                  long long n, bool euler, double s, cudaStream_t st, const GatherSrc* gs, double* mpart) {
   using namespace x32;
   const long long ncol = n * K;
   GatherSrc g{};
   if (gs) g = *gs;
   kb1<<<(unsigned)(n * (P / PB1)), 288, PB1 * 24 * ZS * 16, st>>>(G, scratch_a);
   kb2<<<(unsigned)((ncol + PB2 - 1) / PB2), 192, PB2 * (P + K) * H * 16, st>>>(scratch_a, scratch_b, ncol, c.p.project_mass);
-  kb3<<<(unsigned)(n * (N / PL8)), 256, PL8 * N * RS * 16, st>>>(scratch_b, fin, out, euler ? 1 : 0, s, g, gs ? 1 : 0);
+  kb3<<<(unsigned)(n * (N / PL8)), 256, PL8 * N * RS * 16, st>>>(scratch_b, fin, out, euler ? 1 : 0, s, g, gs ? 1 : 0,
+                                                                  mpart, c.p.L, 2.0 * c.p.L / N);
   c.launches += 3;
 }
 

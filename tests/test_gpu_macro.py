@@ -223,3 +223,66 @@ def test_abi_rejects_invalid_arguments(cuda_device):
     col.transport_setup((3, 1, 1), 1, 1)
     col.bgk_step(f, g, 0.1)
     B.fks_sync(h)
+
+
+# ---------------- NEXT-1: moments fused into the fks_step epilogue (fks_step_moments) ------------------------------
+
+@pytest.mark.parametrize("N,shape,cfl,path", [(32, (4, 3, 2), (1, 1), B.FKS_PATH_AUTO),     # fast path, fused gather
+                                               (32, (2, 2, 2), (0, 1), B.FKS_PATH_AUTO),     # fast path, no transport
+                                               (24, (3, 2, 2), (1, 2), B.FKS_PATH_AUTO),     # small-N path
+                                               (16, (3, 2, 1), (2, 1), B.FKS_PATH_GENERIC)])  # generic path
+def test_step_moments(cuda_device, N, shape, cfl, path):
+    """fks_step_moments: f_out bit-identical to fks_step's (two handles, same inputs and generic-cell history, two
+    consecutive steps), U and W of f_out against the oracle's moments of the same f_out (Eq. DM_update P:464-493:
+    the per-step moments of the new state) and against fks_moments(f_out)."""
+    n = int(np.prod(shape))
+    f = torch.as_tensor(_random_two_maxwellian(n, N, L_BOX, 300 + N), device=cuda_device)
+    a = B.Collision(N, L_BOX, 16, 16, 0, path=path)
+    b = B.Collision(N, L_BOX, 16, 16, 0, path=path)
+    a.transport_setup(shape, *cfl)
+    b.transport_setup(shape, *cfl)
+    s = 0.05
+    cur = f
+    for _ in range(2):
+        out_a, out_b = torch.empty_like(cur), torch.empty_like(cur)
+        a.step(cur, out_a, s)
+        U, W = b.step_moments(cur, out_b, s)
+        torch.cuda.synchronize()
+        assert torch.equal(out_a, out_b)
+        fo = out_b.cpu().numpy()
+        _check_moments(fo, U.cpu().numpy(), W.cpu().numpy(), N, L_BOX)
+        Um, Wm = b.moments(out_b)
+        torch.cuda.synchronize()
+        assert np.all(np.abs(U.cpu().numpy() - Um.cpu().numpy()) <= TOL_U * _phi_abs_scale(fo, N, L_BOX))
+        cur = out_b
+
+
+def test_step_moments_c3_bench_cells(cuda_device):
+    """At the bench configuration's velocity grid (c3: N = 32, M = 32, CFL 1, fused gather) on a 4 x 4 x 2 box:
+    the moments of the new state, and the collision's conservation (mass of every cell's increment ~ 0, so the box
+    mass in U equals the transported input's mass)."""
+    cfg = CONFIGS["c3"]
+    shape = (4, 4, 2)
+    f = inputs.make_f(cfg, device=cuda_device, cells=list(range(32)))
+    col = B.Collision(cfg.N, cfg.L, cfg.M, cfg.M_r, cfg.kernel)
+    col.transport_setup(shape, cfg.cfl_num, cfg.cfl_den)
+    out = torch.empty_like(f)
+    U, W = col.step_moments(f, out, cfg.coll_scale)
+    torch.cuda.synchronize()
+    fo = out.cpu().numpy()
+    _check_moments(fo, U.cpu().numpy(), W.cpu().numpy(), cfg.N, cfg.L)
+    Uin = o.moments(f.cpu().numpy(), cfg.N, cfg.L)
+    assert abs(U[:, 0].sum().item() - Uin[:, 0].sum()) <= 1e-12 * Uin[:, 0].sum()
+
+
+def test_step_moments_argument_checks(cuda_device):
+    col = B.Collision(16, L_BOX, 16, 16, 0)
+    col.transport_setup((2, 1, 1), 1, 1)
+    f = torch.rand(2, 16, 16, 16, dtype=torch.float64, device=cuda_device)
+    out = torch.empty_like(f)
+    with pytest.raises(B.FksError) as ei:
+        B.fks_step_moments(col.h, f, out, 0.1, None, None)
+    assert ei.value.status == B.FKS_ERR_INVALID
+    with pytest.raises(B.FksError) as ei:   # U overlapping f_out
+        B.fks_step_moments(col.h, f, out, 0.1, out, None)
+    assert ei.value.status == B.FKS_ERR_INVALID

@@ -16,7 +16,7 @@ path = os.environ.get("FKS_LIB") or os.path.join(os.path.dirname(os.path.dirname
 lib = C.CDLL(path)
 lib.fks_collision_init.argtypes = [C.POINTER(C.c_void_p), C.c_int, C.c_double, C.c_int, C.c_int, C.c_int]
 lib.fks_collision_batch.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_longlong, C.c_void_p]
-cfg = CONFIGS["c3"]
+cfg = CONFIGS[os.environ.get("FKS_CFG", "c3")]
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 4320
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 5
 f = inputs.make_f(cfg, device="cuda", cells=list(range(n)))
@@ -34,5 +34,6 @@ for _ in range(reps):
     e1.record()
     torch.cuda.synchronize()
     ts.append(e0.elapsed_time(e1))
-print(f"lib {os.path.basename(path)} cells {n}: {np.median(ts):.2f} ms -> full c3 {np.median(ts) * 32768 / n:.1f} ms; "
+print(f"lib {os.path.basename(path)} {cfg.name} cells {n}: {np.median(ts):.3f} ms -> full {cfg.name} "
+      f"{np.median(ts) * cfg.n_cells / n:.3f} ms; "
       f"checksum {Q[:256].abs().sum().item():.15e}")
