@@ -150,6 +150,15 @@ fks_status fks_transport_step_slab(fks_ctx* h, const double* const* planes, doub
 /* Slab variant of fks_step: the gather above, then collision + Euler on the local cells in place in f_out. */
 fks_status fks_step_slab(fks_ctx* h, const double* const* planes, double* f_out, double coll_scale, void* stream);
 
+/* Part of a slab step: destination x-planes [lx0, lx1) of this rank (local indices, 0 <= lx0 <= lx1 <= nx_local)
+ * with the shift of the current step.  advance = 1 starts a new step (advances the generic cell, as fks_step_slab
+ * does); advance = 0 continues it with the same shift (FKS_ERR_STATE if no step was started).  Destination planes
+ * [H, nx_local - H) read only this rank's own planes and are never read by a neighbour, so they can run before
+ * the inter-rank barrier of the step and the boundary planes after it (the paper's relaxation of interior cells
+ * overlapping the exchange).  fks_step_slab = fks_step_slab_range(0, nx_local, advance = 1). */
+fks_status fks_step_slab_range(fks_ctx* h, const double* const* planes, double* f_out, double coll_scale, int lx0,
+                               int lx1, int advance, void* stream);
+
 /* Macroscopic moments per cell ("ToConservative" / "ToPrimitive"):
  *   U[c] = sum_k phi(v_k) f[c][k] dv^3 = (rho, rho u_x, rho u_y, rho u_z, E),  phi = (1, v, |v|^2/2), dv = 2L/N;
  *   W[c] = (rho, u_x, u_y, u_z, T) with (3/2) rho T = E - rho |u|^2 / 2.

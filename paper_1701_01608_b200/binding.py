@@ -26,7 +26,7 @@ EXPORTS = ["fks_collision_init", "fks_collision_init_ex", "fks_collision_batch",
            "fks_get_tables", "fks_get_last_shift", "fks_profile", "fks_profile_read", "fks_debug_timestamps", "fks_launch_count",
            "fks_sync", "fks_destroy", "fks_last_error", "fks_moments", "fks_bgk_batch", "fks_bgk_step",
            "fks_transport_setup_slab", "fks_slab_halo", "fks_slab_plane_count", "fks_transport_step_slab",
-           "fks_step_slab", "fks_step_moments"]
+           "fks_step_slab", "fks_step_moments", "fks_step_slab_range"]
 
 
 class fks_params(C.Structure):
@@ -75,6 +75,7 @@ def load_library(path: str = None):
         "fks_slab_plane_count": ([vp, C.POINTER(i)], i),
         "fks_transport_step_slab": ([vp, vp, vp, vp], i),
         "fks_step_slab": ([vp, vp, vp, d, vp], i),
+        "fks_step_slab_range": ([vp, vp, vp, d, i, i, i, vp], i),
         "fks_bgk_batch": ([vp, vp, vp, d, ll, vp], i),
         "fks_bgk_step": ([vp, vp, vp, d, vp, vp, vp], i),
         "fks_get_info": ([vp, C.POINTER(i), C.POINTER(i), dp, dp], i),
@@ -205,6 +206,11 @@ def fks_transport_step_slab(h: int, planes, f_out, stream=None):
 
 def fks_step_slab(h: int, planes, f_out, coll_scale: float, stream=None):
     _check(load_library().fks_step_slab(h, _plane_array(h, planes), _ptr(f_out), coll_scale, _stream(stream)))
+
+
+def fks_step_slab_range(h: int, planes, f_out, coll_scale: float, lx0: int, lx1: int, advance: bool, stream=None):
+    _check(load_library().fks_step_slab_range(h, _plane_array(h, planes), _ptr(f_out), coll_scale, lx0, lx1,
+                                              1 if advance else 0, _stream(stream)))
 
 
 def fks_moments(h: int, f, U=None, W=None, n_cells: int | None = None, stream=None):

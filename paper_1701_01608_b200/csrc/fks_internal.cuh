@@ -77,6 +77,8 @@ struct Ctx {
   PhaseTimer prof;
   int num_sms = 148;
   int small_ctas = 0;                   // small-N fast path (N = 16, 24): persistent CTAs (SMs x CTAs per SM)
+  Shift slab_shift{};                   // fks_step_slab_range: the shift of the step in progress
+  bool slab_shift_valid = false;
   double* d_mpart = nullptr;            // fks_step_moments: per-CTA partial moment sums of the last kernel
   size_t mpart_elems = 0;
 };
@@ -137,7 +139,8 @@ constexpr int kMaxPlanes = 1024;
 struct PlaneTable {
   const double* p[kMaxPlanes];
 };
-fks_status launch_transport_gather_slab(Ctx& c, const PlaneTable& tab, double* fout, const Shift& sh, cudaStream_t st);
+fks_status launch_transport_gather_slab(Ctx& c, const PlaneTable& tab, double* fout, const Shift& sh, cudaStream_t st,
+                                        long long cell0 = 0, long long ncells = -1);
 
 // moments / BGK (macro.cu): mode 0 = moments of fin into U/W, 1 = out = coef (E - fin), 2 = transport by *sh then
 // out = f* + coef (E[f*] - f*).  U, W optional ([n_cells][5]).

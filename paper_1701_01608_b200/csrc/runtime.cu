@@ -408,22 +408,35 @@ fks_status fks_transport_step_slab(fks_ctx* h, const double* const* planes, doub
   return order_end(c, st, rc);
 }
 
-fks_status fks_step_slab(fks_ctx* h, const double* const* planes, double* f_out, double coll_scale, void* stream) {
+fks_status fks_step_slab_range(fks_ctx* h, const double* const* planes, double* f_out, double coll_scale, int lx0,
+                               int lx1, int advance, void* stream) {
   if (!h) { set_error("NULL handle"); return FKS_ERR_INVALID; }
   Ctx& c = *reinterpret_cast<Ctx*>(h);
   if (!std::isfinite(coll_scale)) { set_error("coll_scale must be finite"); return FKS_ERR_INVALID; }
   static thread_local PlaneTable tab;
   fks_status rc;
   if ((rc = slab_table(c, planes, f_out, tab))) return rc;
+  if (lx0 < 0 || lx1 < lx0 || lx1 > c.nx) { set_error("plane range outside [0, nx_local]"); return FKS_ERR_INVALID; }
+  if (!advance && !c.slab_shift_valid) { set_error("no step in progress: the first call of a step must advance"); return FKS_ERR_STATE; }
   if ((rc = sticky_check())) return rc;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if ((rc = order_begin(c, st))) return rc;
-  Shift sh = advance_generic_cell(c);
+  if (advance) {
+    c.slab_shift = advance_generic_cell(c);
+    c.slab_shift_valid = true;
+  }
+  const long long plane = (long long)c.ny * c.nz, cell0 = lx0 * plane, m = (long long)(lx1 - lx0) * plane;
+  const size_t nv = (size_t)c.N * c.N * c.N;
   c.prof.begin(0, st);
-  rc = launch_transport_gather_slab(c, tab, f_out, sh, st);
+  rc = launch_transport_gather_slab(c, tab, f_out, c.slab_shift, st, cell0, m);
   c.prof.end(0, st);
-  if (!rc) rc = run_collision(c, f_out, f_out, (long long)c.nx * c.ny * c.nz, true, coll_scale, st);
+  if (!rc && m > 0) rc = run_collision(c, f_out + cell0 * nv, f_out + cell0 * nv, m, true, coll_scale, st);
   return order_end(c, st, rc);
+}
+
+fks_status fks_step_slab(fks_ctx* h, const double* const* planes, double* f_out, double coll_scale, void* stream) {
+  if (!h) { set_error("NULL handle"); return FKS_ERR_INVALID; }
+  return fks_step_slab_range(h, planes, f_out, coll_scale, 0, reinterpret_cast<Ctx*>(h)->nx, 1, stream);
 }
 
 fks_status fks_transport_step(fks_ctx* h, const double* f_in, double* f_out, void* stream) {

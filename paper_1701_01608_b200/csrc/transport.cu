@@ -55,11 +55,12 @@ fks_status launch_transport_gather(Ctx& c, const double* fin, double* fout, cons
 // pointers) instead of through a separate halo exchange.  Same copy order and bit-exact result as the
 // single-domain gather.
 __global__ void __launch_bounds__(256) transport_gather_slab_kernel(const PlaneTable tab, double* __restrict__ fout,
-                                                                    Shift sh, int x0, int nx_glob, int halo) {
+                                                                    Shift sh, int x0, int nx_glob, int halo,
+                                                                    long long cell0) {
   __shared__ int sx[kMaxN], sy[kMaxN], sz[kMaxN];
   const int N = sh.N;
   const long long nv = (long long)N * N * N;
-  const long long j = blockIdx.x;  // local destination cell (jx_loc * ny + jy) * nz + jz
+  const long long j = cell0 + blockIdx.x;  // local destination cell (jx_loc * ny + jy) * nz + jz
   const int jz = (int)(j % sh.nz), jy = (int)((j / sh.nz) % sh.ny);
   const int jx = x0 + (int)(j / ((long long)sh.nz * sh.ny));  // global plane
   if (threadIdx.x < N) {
@@ -85,11 +86,12 @@ __global__ void __launch_bounds__(256) transport_gather_slab_kernel(const PlaneT
   }
 }
 
-fks_status launch_transport_gather_slab(Ctx& c, const PlaneTable& tab, double* fout, const Shift& sh, cudaStream_t st) {
-  const long long ncells = (long long)c.nx * c.ny * c.nz;
+fks_status launch_transport_gather_slab(Ctx& c, const PlaneTable& tab, double* fout, const Shift& sh, cudaStream_t st,
+                                        long long cell0, long long ncells) {
+  if (ncells < 0) ncells = (long long)c.nx * c.ny * c.nz - cell0;  // local destination cells [cell0, cell0 + ncells)
   if (ncells <= 0) return FKS_OK;
   if (ncells > 0x7fffffffLL) { set_error("transport: too many cells"); return FKS_ERR_INVALID; }
-  transport_gather_slab_kernel<<<(unsigned)ncells, 256, 0, st>>>(tab, fout, sh, c.x0, c.nx_glob, c.halo);
+  transport_gather_slab_kernel<<<(unsigned)ncells, 256, 0, st>>>(tab, fout, sh, c.x0, c.nx_glob, c.halo, cell0);
   c.launches++;
   return cuda_status(cudaPeekAtLastError(), "transport gather (slab)");
 }

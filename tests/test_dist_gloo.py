@@ -128,3 +128,19 @@ def test_two_rank_gloo_slab_tables():
     assert [(r[1], r[2]) for r in res] == [(0, 5), (5, 9)]
     assert all(r[3] for r in res)
     assert res[0][4] == [0, 1] and res[1][4] == [0, 1]
+
+
+@pytest.mark.parametrize("nx,size,H", [(64, 2, 2), (96, 3, 2), (256, 8, 2), (40, 4, 3), (12, 4, 2), (8, 2, 5)])
+def test_interior_planes_never_read_by_neighbours(nx, size, H):
+    """The overlapped slab step computes [H, nx_local - H) before the barrier: those planes must be read by no
+    other rank (their sources are this rank's own planes: every table entry within H of a destination plane)."""
+    for r in range(size):
+        d = D.SlabDomain(nx, 2, 3, r, size)
+        a, b = D.interior_planes(d.nx_local, H)
+        read = D.planes_read_by_others(d, H)
+        assert not (set(range(a, b)) & read), (r, a, b, sorted(read))
+        for lx in range(a, b):  # sources of an interior plane are own planes
+            for dx in range(-H, H + 1):
+                assert 0 <= lx - dx < d.nx_local
+        if d.nx_local > 2 * H and size > 1:
+            assert read == set(range(0, min(H, d.nx_local))) | set(range(max(0, d.nx_local - H), d.nx_local))

@@ -38,9 +38,12 @@ def _reference(cfg, shape, cfl, f, steps, transport_only):
 
 
 @pytest.mark.parametrize("name,shape,cfl,size", [("c0", (6, 2, 2), (3, 2), 2), ("c0", (7, 1, 2), (3, 2), 3),
-                                                 ("c0", (5, 2, 1), (1, 1), 5), ("c2", (4, 2, 1), (1, 1), 2)])
+                                                 ("c0", (5, 2, 1), (1, 1), 5), ("c2", (4, 2, 1), (1, 1), 2),
+                                                 ("c0", (12, 1, 2), (1, 1), 2), ("c2", (10, 1, 1), (1, 1), 2)])
 @pytest.mark.parametrize("transport_only", [True, False])
 def test_slab_emulated_ranks_bit_exact(cuda_device, name, shape, cfl, size, transport_only):
+    """The last two shapes have interior planes (nx_local > 2H): the overlapped step (interior planes before the
+    barrier, boundary planes after, fks_step_slab_range) must give the same bits as the single-domain step."""
     cfg = CONFIGS[name]
     nx, ny, nz = shape
     n = nx * ny * nz
@@ -60,6 +63,36 @@ def test_slab_emulated_ranks_bit_exact(cuda_device, name, shape, cfl, size, tran
         got = torch.cat(outs)
         torch.cuda.synchronize()
         assert torch.equal(got, ref[s]), (s, (got - ref[s]).abs().max().item())
+
+
+def test_slab_range_checks_and_split(cuda_device):
+    """fks_step_slab_range: a step must start with advance = 1; ranges are checked; splitting a step into
+    interior-then-boundary ranges equals fks_step_slab bit for bit (one rank owning the whole periodic box)."""
+    cfg = CONFIGS["c0"]
+    nx, ny, nz = 8, 1, 2
+    f = inputs.make_f(cfg, device=cuda_device, cells=[c % cfg.n_cells for c in range(nx * ny * nz)])
+    outs = []
+    for split in (False, True):
+        col = B.Collision(cfg.N, cfg.L, cfg.M, cfg.M_r, cfg.kernel)
+        B.fks_transport_setup_slab(col.h, nx, ny, nz, 0, nx, 1, 1)
+        H = B.fks_slab_halo(col.h)
+        table = [f[((x % nx) * ny * nz):((x % nx) + 1) * ny * nz].data_ptr() for x in range(-H, nx + H)]
+        g = torch.empty_like(f)
+        if not split:
+            B.fks_step_slab(col.h, table, g, cfg.coll_scale)
+        else:
+            with pytest.raises(B.FksError) as ei:
+                B.fks_step_slab_range(col.h, table, g, cfg.coll_scale, 0, 2, False)
+            assert ei.value.status == B.FKS_ERR_STATE
+            with pytest.raises(B.FksError) as ei:
+                B.fks_step_slab_range(col.h, table, g, cfg.coll_scale, 3, nx + 1, True)
+            assert ei.value.status == B.FKS_ERR_INVALID
+            B.fks_step_slab_range(col.h, table, g, cfg.coll_scale, H, nx - H, True)
+            B.fks_step_slab_range(col.h, table, g, cfg.coll_scale, 0, H, False)
+            B.fks_step_slab_range(col.h, table, g, cfg.coll_scale, nx - H, nx, False)
+        torch.cuda.synchronize()
+        outs.append(g)
+    assert torch.equal(outs[0], outs[1])
 
 
 def test_slab_argument_checks(cuda_device):
