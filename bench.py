@@ -330,6 +330,8 @@ def main():
                     help="N ranks run ONE periodic box of N x 32 x-planes, slab-decomposed in x (fks_step_slab: the "
                          "transport gathers across slab boundaries from the neighbours' memory over NVLink, one "
                          "barrier per step) instead of N independent boxes")
+    ap.add_argument("--no-decomposed-extra", action="store_true",
+                    help="N > 1: skip the extra slab-decomposed measurement reported under 'decomposed'")
     ap.add_argument("--workload", default="boltzmann", choices=["boltzmann", "bgk"],
                     help="bgk: the BGK-operator FKS step (SURVEY §8(f) NEXT-3; HBM-bound) on the same config")
     args = ap.parse_args()
@@ -442,18 +444,50 @@ def main():
     hot_ms = ph_ms[2] / max(1, ph_cnt[2])
     cells_per_launch = cfg.n_cells * args.steps / max(1, ph_cnt[2])
     achieved = fl["hot"] * cells_per_launch / (hot_ms / 1e3) / 1e12
-    peak = fp64_peak_tflops(1965.0)
     clocks = clk.summary()
-    # DRAM traffic of the dominant kernel from the committed ncu --set full capture (per cell, scaled to this
-    # run's cells per launch); null when no capture of the current kernel is committed
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "r01i_hot_kernel_traffic.json")
+    # FP64 unit-count peak at the SM clock observed under load (median of the samples), max clock if unsampled
+    sm_used = clocks.get("sm_mhz") or 1965.0
+    peak = fp64_peak_tflops(sm_used)
+    # DRAM traffic of the dominant kernel from the committed ncu --set full capture of this kernel (per cell,
+    # scaled to this run's cells per launch); null when no capture of the current kernel is committed
+    traffic, traffic_src = None, None
+    tpath = os.path.join(ROOT, "profiles", f"r02_hot_kernel_traffic_N{cfg.N}.json")
     if os.path.exists(tpath) and col.info.get("path") == 2:
         try:
             tj = json.load(open(tpath))
             traffic = tj["dram_bytes_per_cell"] * cells_per_launch
+            traffic_src = f"profiles/{os.path.basename(tpath)}: {tj.get('source', '')}"
         except Exception:
             traffic = None
+
+    # N > 1: the same workload once more through the slab-decomposed path (one global box of ws x 32 x-planes,
+    # transport gathering across slab boundaries from the neighbours' memory, interior planes before the
+    # per-step barrier): the multi-GPU data path the paper's MPI FKS exercises
+    decomposed = None
+    if ws > 1 and not args.decomposed and not args.no_decomposed_extra:
+        try:
+            dom = D.SlabDomain(cfg.shape[0] * ws, cfg.shape[1], cfg.shape[2], rank, ws)
+            dcol = B.Collision(cfg.N, cfg.L, cfg.M, cfg.M_r, cfg.kernel)
+            dst = D.SlabStepper(dcol, dom, fa, fb, cfg.cfl_num, cfg.cfl_den, barrier=D.stream_barrier(dev))
+            for _ in range(min(args.warmup, 2)):
+                dst.step(s)
+            torch.cuda.synchronize()
+            barrier()
+            d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            d0.record(stream)
+            for _ in range(args.steps):
+                dst.step(s)
+            d1.record(stream)
+            torch.cuda.synchronize()
+            barrier()
+            dms = D.max_over_ranks(d0.elapsed_time(d1), dev) / args.steps
+            decomposed = {"value": D.weak_value(cfg.n_cells, cfg.N ** 3, ws, dms), "unit": unit, "ms_per_step": dms,
+                          "box": f"{cfg.shape[0] * ws}x{cfg.shape[1]}x{cfg.shape[2]} cells, x-slab of "
+                                 f"{dom.nx_local} planes per rank, halo {dst.H}", "scaling": "weak",
+                          "api": "fks_step_slab_range (interior planes, barrier, boundary planes)"}
+            del dst, dcol
+        except Exception as ex:  # report, never lose the main line
+            decomposed = {"error": f"{type(ex).__name__}: {ex}"[:300]}
 
     # end to end through the host-buffer C-ABI call (pinned host memory, copies inside the timed region)
     e2e = None
@@ -494,13 +528,21 @@ def main():
         "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": workload,
         "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "traffic_note": "dram__bytes_read+write per launch from profiles/r01i_hot_kernel_traffic.json "
-                                     "(ncu --set full of this kernel in this bench command), scaled to cells per launch",
-                     "kernel": "term loop (a3-a5: table product, pruned 3D inverse, gain-loss accumulate)",
+                     "traffic_note": ("dram__bytes_read+write per launch, " + traffic_src +
+                                      " (one ncu --set full capture of this kernel), scaled to cells per launch")
+                                     if traffic_src else "no committed ncu capture of this kernel",
+                     "kernel": ("term loop (a3-a5): " + ("hot_kernel_v4, 12-CTA teams" if cfg.N == 32 else
+                                "small_term_kernel, one CTA per (cell, z-class, term chunk)")),
                      "flop_per_cell": fl["hot"], "cells_per_launch": cells_per_launch, "ms_per_launch": hot_ms,
                      "frac_of_measured_dfma": achieved / 33.613,
-                     "peak_note": "FP64 DFMA: 148 SM x 64 lanes x 2 flop x 1965 MHz (unit counts, max clock); "
-                                  "measured DFMA microbench 33.6 TF/s (profiles/r01_box_microbench.jsonl)"},
+                     "peak_at_max_clock": fp64_peak_tflops(1965.0),
+                     # the N = 32 kernel has shown two stable operating points from build to build (about 160 and
+                     # 170 ms per 10 923-cell launch): record which one this build landed on
+                     "operating_point": (("fast" if hot_ms / cells_per_launch * 10923 < 165.0 else "slow")
+                                         if cfg.N == 32 and col.info.get("path") == 2 else None),
+                     "peak_note": f"FP64 DFMA unit counts: 148 SM x 64 lanes x 2 flop x {sm_used:.0f} MHz (median SM "
+                                  "clock sampled under load); measured DFMA microbench 33.6 TF/s "
+                                  "(profiles/r01_box_microbench.jsonl)"},
         "whole_step": {"flop_per_cell": fl["total"],
                        "tflops": fl["total"] * cells_all / ws / (ms_step / 1e3) / 1e12,
                        "frac_of_fp64_peak": fl["total"] * cells_all / ws / (ms_step / 1e3) / 1e12 / peak,
@@ -509,7 +551,7 @@ def main():
                                "term_loop": ph_ms[2] / args.steps, "back": ph_ms[3] / args.steps},
         "path": {1: "generic", 2: "fast"}.get(col.info.get("path"), None),
         "fast_layout": {"ctas_per_cell": col.info.get("ctas_per_cell"), "concurrent_cells": col.info.get("concurrent_cells")},
-        "clocks": clocks, "gpu_launches": launches, "e2e": e2e,
+        "clocks": clocks, "gpu_launches": launches, "e2e": e2e, "decomposed": decomposed,
         "cpu_baseline": {"value": cpu["value"], "unit": unit, "cores": cpu["threads"], "kind": "oracle",
                          "host": host_cpu(),
                          "sample": f"{cpu['cells']} sampled cells of {cfg.name}, collision+Euler, "
