@@ -324,7 +324,9 @@ __global__ void __launch_bounds__(32 * WARPS, N == 16 ? 2 : 1) small_term_kernel
     }
     const double2* fh = A.fhT + cell * (long long)(K * NLOW);
 
+#ifdef FKS_SMALL_PHASE_TIMING
     int dstep = 0;
+#endif
     // phase runner: X items of class xr (-1: skip X), Z items of term zt (-1: skip Z), Y items of class yr
     auto run_phase = [&](int ph, int zt, int xr, int xb, int yr, int yb) {
 #pragma unroll 1
@@ -352,10 +354,14 @@ __global__ void __launch_bounds__(32 * WARPS, N == 16 ? 2 : 1) small_term_kernel
           else x_task<N, 2>(W2b, col, pen);
         }
       }
+#ifdef FKS_SMALL_PHASE_TIMING  // tools/phase_timing_small.py (a build variant: the stamps are not in the product)
       if (A.dbg && u == blockIdx.x && blockIdx.x < 32 && lane == 0 && dstep < 64) A.dbg[((long long)blockIdx.x * 16 + warp) * 128 + 2 * dstep] = clock64();
       __syncthreads();
       if (A.dbg && u == blockIdx.x && blockIdx.x < 32 && lane == 0 && dstep < 64) A.dbg[((long long)blockIdx.x * 16 + warp) * 128 + 2 * dstep + 1] = clock64();
       dstep++;
+#else
+      __syncthreads();
+#endif
     };
 
     // phase sequence (ONE call site of run_phase keeps one copy of every task body in the kernel):

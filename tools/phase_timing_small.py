@@ -1,6 +1,7 @@
 """Per-phase cycle counts of the small-N term kernel (FKS_PHASE_TIMING=1): for the first unit of CTAs 0..31, every
 warp's busy time (work before the phase barrier) and the phase length (barrier exit to barrier exit).
-Usage: python tools/phase_timing_small.py [config]"""
+Needs the instrumented build: FKS_LIB=$(python tools/build_variant.py ptime -DFKS_SMALL_PHASE_TIMING) python
+tools/phase_timing_small.py [config]"""
 import os
 import sys
 
