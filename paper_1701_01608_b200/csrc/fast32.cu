@@ -36,14 +36,14 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t a = (uint32_t)__cvta_generic_to_shared(bar);
   uint32_t done = 0;
   unsigned ns = 32;
-  long long spins = 0;
+  unsigned spins = 0;
   while (true) {
     asm volatile("{ .reg .pred p; mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
                  : "=r"(done) : "r"(a), "r"(parity) : "memory");
     if (done) break;
     __nanosleep(ns);
     if (ns < 1024) ns <<= 1;
-    if (++spins > (1LL << 24)) asm volatile("trap;");  // never hang the GPU on a byte-count bug
+    if (++spins > (1u << 24)) asm volatile("trap;");  // never hang the GPU on a byte-count bug
   }
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -105,16 +105,22 @@ struct Args {
   long long* dbg;        // optional per-phase clock64 stamps (tools/phase_timing.py); nullptr in production
 };
 
+#ifdef FKS_V4_PHASE_TIMING
+#define STAMP(i) do { if (st) st[i] = clock64(); } while (0)
+#else
+#define STAMP(i) do { } while (0)
+#endif
+
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
 __device__ __forceinline__ void poll_ge(const unsigned* p, unsigned target) {
-  long long spins = 0;
+  unsigned spins = 0;
   while (ld_acquire(p) < target) {
     __nanosleep(128);
-    if (++spins > (1LL << 25)) asm volatile("trap;");  // never hang the GPU on a counting bug
+    if (++spins > (1u << 25)) asm volatile("trap;");  // never hang the GPU on a counting bug
   }
 }
 // publication of W1 by one thread after a named barrier: release semantics are cumulative over the stores the
@@ -220,8 +226,11 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
   double2* W1t = A.W1 + (long long)team * NB * W1_BUF;
   unsigned* zcnt = A.ctr + (long long)team * CTR_STRIDE;  // + 32 b
   unsigned* ycnt = zcnt + 32 * NB;                         // + 32 b
-  const long long ncell_team = (team < A.n_cells) ? (A.n_cells - 1 - team) / A.nteams + 1 : 0;
-  const long long total_tg = ncell_team * A.T1;
+  // 32-bit loop state (a launch covers one workspace chunk: far fewer than 2^31 cell-terms per team); 64-bit
+  // counters spilled to local memory in the YX warps and their reloads stalled the term loop
+  const int ncells = (int)A.n_cells;
+  const int ncell_team = (team < ncells) ? (ncells - 1 - team) / A.nteams + 1 : 0;
+  const int total_tg = ncell_team * A.T1;
 
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;"
@@ -266,48 +275,50 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
     int* xc = s_xc[g];
     auto wait_ge = [&](const int* ptr, int target) {
       if (lane == 0) {
-        long long spins = 0;
+        unsigned spins = 0;
         unsigned ns = 32;
         while (vload(ptr) < target) {
           __nanosleep(ns);
           if (ns < 512) ns <<= 1;
-          if (++spins > (1LL << 26)) asm volatile("trap;");
+          if (++spins > (1u << 26)) asm volatile("trap;");
         }
       }
       __syncwarp();
     };
-    auto issue_w1 = [&](long long tgi) {
-      const double2* src = W1t + (tgi % NB) * (long long)W1_BUF + (long long)pz0 * NPEN;
+    auto issue_w1 = [&](int tgi) {
+      const double2* src = W1t + (tgi % NB) * (long long)W1_BUF + pz0 * NPEN;
       asm volatile("fence.proxy.async.global;" ::: "memory");
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_expect(&bar_w1[g], 2u * W1IN_B);
       bulk_g2s(in0, src, W1IN_B, &bar_w1[g]);
       bulk_g2s(in1, src + NPEN, W1IN_B, &bar_w1[g]);
     };
-    auto try_issue_w1 = [&](long long tz, bool block) {  // lane 0: bulk-copy W1(tz) once per group
+    auto try_issue_w1 = [&](int tz, bool block) {  // lane 0: bulk-copy W1(tz) once per group
       if (tz >= total_tg) return;
-      if (vload(&s_w1iss[g]) > (int)tz) return;
-      if (vload(&s_yall[g]) < 3 * (int)tz) {
+      if (vload(&s_w1iss[g]) > tz) return;
+      if (vload(&s_yall[g]) < 3 * tz) {
         if (!block) return;
-        long long spins = 0;
-        while (vload(&s_yall[g]) < 3 * (int)tz) { __nanosleep(64); if (++spins > (1LL << 26)) asm volatile("trap;"); }
+        unsigned spins = 0;
+        while (vload(&s_yall[g]) < 3 * tz) { __nanosleep(64); if (++spins > (1u << 26)) asm volatile("trap;"); }
       }
       unsigned* zc = zcnt + 32 * (tz % NB);
       const unsigned target = (unsigned)(TM * (tz / NB + 1));
       if (block) poll_ge(zc, target);
       else if (ld_acquire(zc) < target) return;
-      if (atomicCAS(&s_w1iss[g], (int)tz, (int)tz + 1) == (int)tz) issue_w1(tz);
+      if (atomicCAS(&s_w1iss[g], tz, tz + 1) == tz) issue_w1(tz);
     };
     uint32_t par = 0;
-    long long tg = 0;
+    int tg = 0;
 #pragma unroll 1
-    for (long long cell = team; cell < A.n_cells; cell += A.nteams) {
+    for (int cell = team; cell < ncells; cell += A.nteams) {
 #pragma unroll 1
       for (int t = 0; t < A.T1; t++, tg++) {
-        const int T = (int)tg;
+        const int T = tg;
+#ifdef FKS_V4_PHASE_TIMING  // tools/phase_timing_v4.py: an instrumented build variant only
         long long* st = (A.dbg && lane == 0 && warp == 6 && cell == team && t >= 2 && t < 6)
                             ? A.dbg + (long long)blockIdx.x * 128 + (t - 2) * 16 : nullptr;
-        if (st) st[0] = clock64();
+#endif
+        STAMP(0);
         if (!isx) {
           // ---------------- Y warp ----------------
           if (lane == 0 && c == 0) try_issue_w1(tg, true);
@@ -316,7 +327,7 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
             __threadfence();
             atomicAdd(ycnt + 32 * (tg % NB), 1u);  // this group has consumed W1(tg)
           }
-          if (st) st[1] = clock64();
+          STAMP(1);
           wait_ge(&xc[c], T);  // slot c: X(g, c) of term t-1 has parked its rows
 #pragma unroll 1
           for (int pl = 0; pl < 2; pl++) {
@@ -334,7 +345,7 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
             atomicAdd(&yc[c], 1);
             if (atomicAdd(&s_yall[g], 1) + 1 == 3 * (T + 1)) try_issue_w1(tg + 1, false);  // prefetch
           }
-          if (st) st[2] = clock64();
+          STAMP(2);
         } else {
           // ---------------- X warp ----------------
           wait_ge(&yc[c], T + 1);
@@ -424,25 +435,27 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
     double2* zm = reinterpret_cast<double2*>(smem + OFF_Z + ZBLK_B);
     double2* fh = reinterpret_cast<double2*>(smem + OFF_Z + 2 * ZBLK_B);  // the cell's f^ block (TMA, per cell)
     const uint32_t fblk = (uint32_t)(K * nh) * 16u;
-    auto issue_fh = [&](long long cl) {
+    auto issue_fh = [&](int cl) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_expect(&bar_fh, fblk);
       bulk_g2s(fh, A.fhatT + cl * (long long)LHN + K * h0, fblk, &bar_fh);
     };
     if (zt == 0 && ncell_team > 0) issue_fh(team);
     uint32_t par_fh = 0;
-    long long tg = 0;
+    int tg = 0;
 #pragma unroll 1
-    for (long long cell = team; cell < A.n_cells; cell += A.nteams) {
+    for (int cell = team; cell < ncells; cell += A.nteams) {
       mbar_wait(&bar_fh, par_fh);
       par_fh ^= 1;
 #pragma unroll 1
       for (int t = 0; t < A.T1; t++, tg++) {
         const double2* tb = A.tabT + (long long)t * LHN + K * h0;     // the member's table block (L2)
+#ifdef FKS_V4_PHASE_TIMING
         long long* st = (A.dbg && zt == 0 && cell == team && t >= 2 && t < 6)
                             ? A.dbg + (long long)blockIdx.x * 128 + (t - 2) * 16 + 8 : nullptr;
-        if (st) st[0] = clock64();
-        if (st) st[1] = clock64();
+#endif
+        STAMP(0);
+        STAMP(1);
         // products: Z = (a + ib) f^ for the staged pencils, and for their mirrors (-lx,-ly): (a + ib) conj(f^)
         // at the reversed lz (a, b even; f real)
         {  // element pairs {i, 30 - i} of pencil j, e = i * nh + j; i = e / nh by multiply-high (exact: e nh < 2^32).
@@ -483,7 +496,7 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
           }
         }
         nbar(3, NZT);  // products complete (after the cell's last term the f^ block is free)
-        if (zt == 0 && t == A.T1 - 1 && cell + A.nteams < A.n_cells) issue_fh(cell + A.nteams);
+        if (zt == 0 && t == A.T1 - 1 && cell + A.nteams < ncells) issue_fh(cell + A.nteams);
         // publish W1(tg - 2) and W1(tg - 1) every second term: one store drain per pair (it costs ~1.4 K cycles
         // on the Z warps, which set the period; the consumers have slack)
         if (zt == 0 && tg >= 2 && (tg & 1) == 0) {
@@ -491,12 +504,12 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
           atomicAdd(zcnt + 32 * ((tg - 2) % NB), 1u);
           atomicAdd(zcnt + 32 * ((tg - 1) % NB), 1u);
         }
-        if (st) st[2] = clock64();
+        STAMP(2);
         if (zt == 0) {
           if (tg >= NB) poll_ge(ycnt + 32 * (tg % NB), (unsigned)(2 * TM * (tg / NB)));  // buffer free
         }
         nbar(3, NZT);
-        if (st) st[3] = clock64();
+        STAMP(3);
         double2* W1b = W1t + (tg % NB) * (long long)W1_BUF;
         {  // 4 Z warps: single class tasks tau = r * na + j, 2 rounds of 128 threads cover 3 na <= 246
           const int na = nh + nmir;
@@ -518,7 +531,7 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
           }
         }
         nbar(3, NZT);
-        if (st) st[4] = clock64();
+        STAMP(4);
       }
     }
     if (zt == 0 && tg > 0) {  // publish what is left (tg even: W1(tg-2), W1(tg-1); tg odd: W1(tg-1))

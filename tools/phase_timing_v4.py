@@ -1,4 +1,4 @@
-"""Per-phase cycle counts of the v4 term-loop kernel (FKS_PHASE_TIMING=1): YX group 0 and Z warps of every CTA,
+"""Per-phase cycle counts of the v4 term-loop kernel (FKS_PHASE_TIMING=1; needs the instrumented build variant: FKS_LIB=$(python tools/build_variant.py ptime4 -DFKS_V4_PHASE_TIMING)): YX group 0 and Z warps of every CTA,
 terms 2..5 of the first cell of each team.  Usage: python tools/phase_timing_v4.py [config] [n_cells]"""
 import os
 import sys
