@@ -413,8 +413,16 @@ def main():
         else:
             col.step(bufs[i % 2], bufs[(i + 1) % 2], s)
 
-    for i in range(args.warmup):
-        one_step(i)
+    # W warm-up steps; on one rank at least 0.3 s of them, so that tiny workloads (c0) are timed at full clocks
+    # (several ranks keep exactly W: the decomposed step has a collective per step)
+    t_w = time.perf_counter()
+    nw = 0
+    while nw < args.warmup or (ws == 1 and time.perf_counter() - t_w < 0.3):
+        one_step(nw)
+        nw += 1
+        if nw >= args.warmup:
+            torch.cuda.synchronize()
+    args.warmup = nw
     torch.cuda.synchronize()
     barrier()
     B.fks_profile(col.h, True)
@@ -536,10 +544,11 @@ def main():
                      "flop_per_cell": fl["hot"], "cells_per_launch": cells_per_launch, "ms_per_launch": hot_ms,
                      "frac_of_measured_dfma": achieved / 33.613,
                      "peak_at_max_clock": fp64_peak_tflops(1965.0),
-                     # the N = 32 kernel has shown two stable operating points from build to build (about 160 and
-                     # 170 ms per 10 923-cell launch): record which one this build landed on
-                     "operating_point": (("fast" if hot_ms / cells_per_launch * 10923 < 165.0 else "slow")
+                     # the N = 32 kernel has shown two stable operating points from build to build (about 444 and
+                     # 472 ns per cell and term: 160 / 170 ms per 10 923-cell c3 launch): record which
+                     "operating_point": (("fast" if hot_ms * 1e6 / (cells_per_launch * (T + 1)) < 457.0 else "slow")
                                          if cfg.N == 32 and col.info.get("path") == 2 else None),
+                     "ns_per_cell_term": hot_ms * 1e6 / (cells_per_launch * (T + 1)),
                      "peak_note": f"FP64 DFMA unit counts: 148 SM x 64 lanes x 2 flop x {sm_used:.0f} MHz (median SM "
                                   "clock sampled under load); measured DFMA microbench 33.6 TF/s "
                                   "(profiles/r01_box_microbench.jsonl)"},
