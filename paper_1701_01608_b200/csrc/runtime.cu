@@ -594,7 +594,10 @@ fks_status fks_step_host(fks_ctx* h, const double* f_in_host, double* f_out_host
   // slabs: more slabs expose less of the first copy-in and the last copy-out (c3: 32 slabs of one plane;
   // measured e2e 1.71e9 with 4 slabs, 1.82e9 with 8, 1.88e9 with 16, 1.90e9 with 32); each
   // slab must be at least max|delta_x| planes wide, and the halo must not wrap onto itself
-  int nslab = 32;
+  // ... and no slab below 32 MB of input: a small box (c1: 7 MB) would otherwise pay a dozen kernel launches
+  // per slab for a copy that takes microseconds
+  const long long box_bytes = (long long)nx * pbytes;
+  int nslab = (int)std::max(1LL, std::min(32LL, box_bytes / (32LL << 20)));
   if (const char* e = std::getenv("FKS_HOST_SLABS")) nslab = std::max(1, std::atoi(e));
   int nch = std::min(nslab, nx / std::max(1, dmax));
   if (nch < 1 || nx <= 2 * dmax) nch = 1;                  // halo too wide for slabs: one piece
