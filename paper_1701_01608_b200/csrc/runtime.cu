@@ -335,6 +335,7 @@ fks_status fks_transport_setup(fks_ctx* h, int nx, int ny, int nz, long long cfl
   std::fill(c.offsets.begin(), c.offsets.end(), 0);
   c.transport_ready = true;
   c.slab = false;
+  c.slab_shift_valid = false;
   c.nx_glob = nx; c.x0 = 0; c.halo = 0;
   return FKS_OK;
 }
@@ -355,6 +356,7 @@ fks_status fks_transport_setup_slab(fks_ctx* h, int nx_global, int ny, int nz, i
   const int H = halo_bound(cfl_num, cfl_den);
   if (nx_local + 2LL * H > kMaxPlanes) { set_error("slab: nx_local + 2*halo exceeds 1024 planes"); return FKS_ERR_UNSUPPORTED; }
   c.slab = true;
+  c.slab_shift_valid = false;
   c.nx_glob = nx_global; c.x0 = x0; c.halo = H;
   return FKS_OK;
 }
@@ -402,6 +404,7 @@ fks_status fks_transport_step_slab(fks_ctx* h, const double* const* planes, doub
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if ((rc = order_begin(c, st))) return rc;
   Shift sh = advance_generic_cell(c);
+  c.slab_shift_valid = false;  // a later fks_step_slab_range(advance = 0) must not reuse an older step's shift
   c.prof.begin(0, st);
   rc = launch_transport_gather_slab(c, tab, f_out, sh, st);
   c.prof.end(0, st);
