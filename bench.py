@@ -69,6 +69,14 @@ class ClockSampler:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
                                           "--format=csv,noheader,nounits", "-lms", "200"],
                                          stdout=self.fh, stderr=subprocess.DEVNULL)
+            # let nvidia-smi initialise (first sample written) before the timed region starts: its start-up
+            # stalled the host thread by tens of ms, which doubled the measured time of short (c1) runs
+            t0 = time.perf_counter()
+            while time.perf_counter() - t0 < 2.0:
+                self.fh.flush()
+                if os.path.getsize(self.path) > 0:
+                    break
+                time.sleep(0.02)
         except Exception:
             self.proc = None
         return self
