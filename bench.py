@@ -550,7 +550,7 @@ def main():
                      "kernel": ("term loop (a3-a5): " + ("hot_kernel_v4, 12-CTA teams" if cfg.N == 32 else
                                 "small_term_kernel, one CTA per (cell, z-class, term chunk)")),
                      "flop_per_cell": fl["hot"], "cells_per_launch": cells_per_launch, "ms_per_launch": hot_ms,
-                     "frac_of_measured_dfma": achieved / 33.613,
+                     "frac_of_measured_dfma": achieved / 36.66,
                      "peak_at_max_clock": fp64_peak_tflops(1965.0),
                      # the N = 32 kernel has shown two stable operating points from build to build (about 444 and
                      # 472 ns per cell and term: 160 / 170 ms per 10 923-cell c3 launch): record which
@@ -558,8 +558,8 @@ def main():
                                          if cfg.N == 32 and col.info.get("path") == 2 else None),
                      "ns_per_cell_term": hot_ms * 1e6 / (cells_per_launch * (T + 1)),
                      "peak_note": f"FP64 DFMA unit counts: 148 SM x 64 lanes x 2 flop x {sm_used:.0f} MHz (median SM "
-                                  "clock sampled under load); measured DFMA microbench 33.6 TF/s "
-                                  "(profiles/r01_box_microbench.jsonl)"},
+                                  "clock sampled under load); measured DFMA 36.66 TF/s with 16 warps per SM "
+                                  "(profiles/r02_dmma_dfma_mix.jsonl; 33.6 with 8 chains in r01_box_microbench)"},
         "whole_step": {"flop_per_cell": fl["total"],
                        "tflops": fl["total"] * cells_all / ws / (ms_step / 1e3) / 1e12,
                        "frac_of_fp64_peak": fl["total"] * cells_all / ws / (ms_step / 1e3) / 1e12 / peak,
