@@ -301,6 +301,18 @@ def test_fast_path_random_and_ragged(cuda_device):
     assert rel_err_per_cell(Q, qg).max() <= TOL_Q
 
 
+def test_fast_path_project_mass(cuda_device):
+    """project_mass (A24: Q^_0 := 0) on the N = 32 fast path: the zero mode is cleared in the back transform's first
+    kernel (kx = 0 plane of the x-transformed G); against the oracle with project_mass, and Σ Q = 0 to rounding."""
+    cfg = CONFIGS["c2"]
+    col = make(cfg, path=B.FKS_PATH_FAST, project_mass=1)
+    f = inputs.make_f(cfg, device=cuda_device, cells=[0, 5, 300, 511])
+    Q = col.collision_batch(f).cpu().numpy()
+    ref = oracle_Q(f.cpu().numpy(), cfg_tables("c2"), project_mass=True)
+    assert rel_err_per_cell(Q, ref).max() <= TOL_Q
+    assert np.abs(Q.reshape(4, -1).sum(1)).max() <= 1e-13 * np.abs(Q).max() * Q[0].size
+
+
 def test_fast_path_mass(cuda_device):
     cfg = CONFIGS["c4"]
     f = inputs.make_f(cfg, device=cuda_device, cells=list(range(16)))
