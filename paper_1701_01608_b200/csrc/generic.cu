@@ -53,7 +53,8 @@ __global__ void __launch_bounds__(256) dft_axis_kernel(AxisArgs A) {
     int m = (int)(((long long)A.sign * (-A.in_off) * vo) % A.M);
     if (m < 0) m += A.M;
     const long long tab0 = (IK == IN_CPLX_TAB) ? base % A.cell_elems : 0;
-    double sr1 = 0.0, si1 = 0.0;  // odd-i partial sums: two independent FMA chains
+    // one accumulation chain in input order, with the same explicit FMAs as dft_tile_kernel: both variants give
+    // the same bits, so results do not depend on which one a batch size (or a workspace chunk) selects
 #pragma unroll 2
     for (int i = 0; i < A.n_in; i++) {
       const long long e = base + (long long)i * A.R;
@@ -68,21 +69,16 @@ __global__ void __launch_bounds__(256) dft_axis_kernel(AxisArgs A) {
         double2 x = reinterpret_cast<const double2*>(A.in)[e];
         xr = x.x; xi = x.y;
         if (IK == IN_CPLX_TAB) {
-          double2 t = A.ab[tab0 + (long long)i * A.R];  // (a, b): (a + i b)(xr + i xi)
-          double zr = t.x * xr - t.y * xi, zi = t.x * xi + t.y * xr;
+          const double2 t = A.ab[tab0 + (long long)i * A.R];  // (a, b): (a + i b)(xr + i xi)
+          const double zr = fma(t.x, xr, -(t.y * xi)), zi = fma(t.x, xi, t.y * xr);
           xr = zr; xi = zi;
         }
       }
-      if (i & 1) {
-        sr1 = fma(xr, w.x, fma(-xi, w.y, sr1));
-        si1 = fma(xr, w.y, fma(xi, w.x, si1));
-      } else {
-        sr = fma(xr, w.x, fma(-xi, w.y, sr));
-        si = fma(xr, w.y, fma(xi, w.x, si));
-      }
+      sr = fma(xr, w.x, fma(-xi, w.y, sr));
+      si = fma(xr, w.y, fma(xi, w.x, si));
     }
-    sr = (sr + sr1) * A.scale;
-    si = (si + si1) * A.scale;
+    sr *= A.scale;
+    si *= A.scale;
     if (OK == OUT_CPLX) {
       reinterpret_cast<double2*>(A.out)[idx] = make_double2(sr, si);
     } else if (OK == OUT_ACC_G) {
@@ -122,7 +118,7 @@ __global__ void __launch_bounds__(256) dft_tile_kernel(AxisArgs A) {
       x = reinterpret_cast<const double2*>(A.in)[e];
       if (IK == IN_CPLX_TAB) {
         const double2 t = A.ab[tab0 + (long long)i * A.R];  // (a, b): (a + i b)(xr + i xi)
-        x = make_double2(t.x * x.x - t.y * x.y, t.x * x.y + t.y * x.x);
+        x = make_double2(fma(t.x, x.x, -(t.y * x.y)), fma(t.x, x.y, t.y * x.x));  // as dft_axis_kernel
       }
     }
     xs[i * 32 + lane] = x;

@@ -286,3 +286,23 @@ def test_step_moments_argument_checks(cuda_device):
     with pytest.raises(B.FksError) as ei:   # U overlapping f_out
         B.fks_step_moments(col.h, f, out, 0.1, out, None)
     assert ei.value.status == B.FKS_ERR_INVALID
+
+
+def test_step_moments_chunked(cuda_device):
+    """fks_step_moments when the step runs in several workspace chunks (max_cells_in_flight): the moment rows of
+    every chunk land at their cells' offsets (fast path, fused gather)."""
+    N, shape = 32, (5, 2, 2)
+    n = int(np.prod(shape))
+    f = torch.as_tensor(_random_two_maxwellian(n, N, L_BOX, 404), device=cuda_device)
+    a = B.Collision(N, L_BOX, 16, 16, 0)
+    b = B.Collision(N, L_BOX, 16, 16, 0, max_cells_in_flight=7)
+    for col in (a, b):
+        col.transport_setup(shape, 1, 1)
+    oa, ob = torch.empty_like(f), torch.empty_like(f)
+    Ua, Wa = a.step_moments(f, oa, 0.05)
+    Ub, Wb = b.step_moments(f, ob, 0.05)
+    torch.cuda.synchronize()
+    assert torch.equal(oa, ob)
+    fo = ob.cpu().numpy()
+    _check_moments(fo, Ub.cpu().numpy(), Wb.cpu().numpy(), N, L_BOX)
+    assert np.abs(Ua.cpu().numpy() - Ub.cpu().numpy()).max() <= TOL_U * _phi_abs_scale(fo, N, L_BOX).max()

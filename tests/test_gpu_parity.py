@@ -418,3 +418,31 @@ def test_collision_batch_host_matches_device(cuda_device, name, n):
     Qp = torch.empty_like(fp)
     B.fks_collision_batch_host(col.h, fp, Qp, n)
     assert torch.equal(Qp, Qd)
+
+
+# ---------------- small-N fast path (N = 16, 24; csrc/small.cu) edge cases ------------------------------------------
+
+def test_small_path_single_cell_and_many_terms(cuda_device):
+    """One cell (3 units on a 148-CTA grid) and many terms: Maxwell molecules with 16 radial nodes and 16 directions
+    at N = 16 (T + 1 = 257, 16 term chunks summed in order) against the oracle."""
+    N = 16
+    col = B.Collision(N, L_BOX, 16, 16, 1)
+    assert B.fks_get_path(col.h) == B.FKS_PATH_FAST
+    f = inputs.random_field(1, N, seed=71, signed=False).to(cuda_device)
+    Q = col.collision_batch(f).cpu().numpy()
+    ref = oracle_Q(f.cpu().numpy(), oracle_tables(N, L_BOX, 16, 16, 1))
+    assert rel_err_per_cell(Q, ref).max() <= TOL_Q
+
+
+def test_small_path_more_units_than_ctas(cuda_device):
+    """c1 velocity grid (N = 24) with 150 cells: 150 x 3 x 16 units over the persistent grid (every CTA runs many
+    units, G zeroed per unit); sampled cells against the oracle, and chunking (max_cells_in_flight) is bit-exact."""
+    cfg = CONFIGS["c1"]
+    f = inputs.random_field(150, cfg.N, seed=5, signed=False).to(cuda_device)
+    col = B.Collision(cfg.N, cfg.L, cfg.M, cfg.M_r, cfg.kernel)
+    Q = col.collision_batch(f)
+    q2 = B.Collision(cfg.N, cfg.L, cfg.M, cfg.M_r, cfg.kernel, max_cells_in_flight=37).collision_batch(f)
+    assert torch.equal(Q, q2)
+    idx = [0, 1, 77, 149]
+    ref = oracle_Q(f[idx].cpu().numpy(), cfg_tables("c1"))
+    assert rel_err_per_cell(Q[idx].cpu().numpy(), ref).max() <= TOL_Q
