@@ -96,7 +96,7 @@ constexpr int CTR_STRIDE = 256;               // counter words per team (one 128
 struct Args {
   const double2* fhatT;  // [cell][LHN], 12 blocks
   const double2* tabT;   // [t][LHN], 12 blocks
-  double* G;             // [cell][px][pz][py]
+  double* G;             // [cell][px][pz/2][py][pz%2]: pairs of z-rows interleaved (the back transform packs them)
   double2* W1;           // [team][NB][P][NPEN]
   unsigned* ctr;         // [team][CTR_STRIDE]: per W1 buffer b: zcnt at 32 b, ycnt at 32 (NB + b) (zeroed)
   long long n_cells;
@@ -413,15 +413,16 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
             g_accumulate(tX + 32u * rx, u);
           }
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-          if (t == A.T1 - 1) {  // G[cell][px = 3q' + rx][pz][py = 3 xq + c]
-            double* Gc = A.G + cell * (long long)(P * P * P) + (long long)(pz0 + xp) * P;
+          if (t == A.T1 - 1) {  // G[cell][px = 3q' + rx][pz / 2][py = 3 xq + c][pz % 2]: z-rows interleaved in pairs
+            const int pz = pz0 + xp;
+            double* Gc = A.G + cell * (long long)(P * P * P) + (long long)(pz >> 1) * (2 * P) + (pz & 1);
 #pragma unroll 1
             for (int rx = 0; rx < 3; rx++) {
               uint32_t gw[32];
               tmem_ld32(tX + 32u * rx, gw);
 #pragma unroll
               for (int q = 0; q < 16; q++)
-                Gc[(long long)(3 * q + rx) * P * P + 3 * xq + c] = __hiloint2double((int)gw[2 * q + 1], (int)gw[2 * q]);
+                Gc[(long long)(3 * q + rx) * P * P + 2 * (3 * xq + c)] = __hiloint2double((int)gw[2 * q + 1], (int)gw[2 * q]);
             }
           }
         }

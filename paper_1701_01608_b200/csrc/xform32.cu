@@ -7,7 +7,7 @@
 //
 //   forward  Kf1 plane jx : f(jx,jy,jz)  --z (real, lz=0..15)--> --y (ly in K')-->  F2[cell][jx][ly][lz]
 //            Kf2 column ly: F2(:,ly,lz)  --x (lx in K'), N^-3-->  f^T[cell][lz][lx*31+ly] and its conjugate at -l
-//   back     Kb1 plane px : G[cell][px][pz][py] --y (real, ky=0..15)--> --z (kz in K')--> H2[cell][px][kz][ky]
+//   back     Kb1 plane px : G[cell][px][pz/2][py][pz%2] --y (real, ky=0..15)--> --z (kz in K')--> H2[cell][px][kz][ky]
 //            Kb2 column kz: H2(:,kz,ky)  --x (kx in K'), P^-3, [Q^_0 := 0]--> --x inverse (jx)--> E1[cell][jx][kz][ky]
 //            Kb3 plane jx : E1(jx,:,:)   --z inverse (jz)--> --y Hermitian->real (jy)-->  Q (or f* + s Q)
 // (G is stored py-fastest so that the term-loop kernel writes it coalesced; the real axis of the back transform
@@ -205,13 +205,12 @@ __global__ void __launch_bounds__(288, 2) kb1(const double* __restrict__ G, doub
   const int tid = threadIdx.x;
   const long long cell = blockIdx.x / (P / PB1);
   const int px0 = (blockIdx.x % (P / PB1)) * PB1;
-  {
-    const double* src = G + (cell * P + px0) * P * P;
-    double* dst = reinterpret_cast<double*>(zc);
+  {  // G holds each pair of z-rows interleaved: (G(2pr, py), G(2pr+1, py)) is one 16-byte element
+    const double2* src = reinterpret_cast<const double2*>(G + (cell * P + px0) * P * P);
 #pragma unroll 4
-    for (int i = tid; i < PB1 * P * P; i += 288) {
-      const int row = i / P, col = i - row * P;  // row = s * 48 + pz, col = py
-      cp8(dst + ((row >> 1) * ZS + col) * 2 + (row & 1), src + i);
+    for (int i = tid; i < PB1 * P * P / 2; i += 288) {
+      const int pr = i / P, col = i - pr * P;  // pr = s * 24 + row pair, col = py
+      cp16(zc + pr * ZS + col, src + i);
     }
   }
   cp_wait_all();
