@@ -54,6 +54,8 @@ struct Ctx {
   // workspace
   void* d_ws = nullptr;
   size_t ws_bytes = 0;
+  long long auto_chunk = 0;             // cells per workspace chunk (max_cells_in_flight = 0), computed once
+  size_t auto_chunk_per_cell = 0;
   long long ws_cells = 0;
   // host-buffer path staging
   double* d_stage_in = nullptr;

@@ -131,13 +131,19 @@ static fks_status order_end(Ctx& c, cudaStream_t st, fks_status rc) {
   return rc ? rc : r2;
 }
 
-static long long chunk_cells(const Ctx& c, size_t per_cell, long long n_cells) {
+static long long chunk_cells(Ctx& c, size_t per_cell, long long n_cells) {
   long long lim = c.p.max_cells_in_flight;
   if (lim <= 0) {
-    size_t fr = 0, tot = 0;
-    if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) { cudaGetLastError(); fr = 8ull << 30; }
-    size_t budget = std::min<size_t>(fr / 3, 24ull << 30);
-    lim = std::max<long long>(1, (long long)(budget / std::max<size_t>(per_cell, 1)));
+    // the memory query is done once per handle and per-cell size (cudaMemGetInfo costs host time on every call,
+    // which small, launch-bound steps (c0) cannot afford); the workspace then stays allocated at that size
+    if (c.auto_chunk <= 0 || c.auto_chunk_per_cell != per_cell) {
+      size_t fr = 0, tot = 0;
+      if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) { cudaGetLastError(); fr = 8ull << 30; }
+      size_t budget = std::min<size_t>(fr / 3, 24ull << 30);
+      c.auto_chunk = std::max<long long>(1, (long long)(budget / std::max<size_t>(per_cell, 1)));
+      c.auto_chunk_per_cell = per_cell;
+    }
+    lim = c.auto_chunk;
   }
   return std::min(lim, n_cells);
 }
