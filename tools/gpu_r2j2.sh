@@ -1,0 +1,8 @@
+set -x
+cd $GRAFT_REPO_ROOT
+FKS_LIB=build_variants/libfks_y4z6.so timeout 600 python -m pytest tests/test_gpu_parity.py tests/test_gpu_step_parity.py -m gpu -x -q -k "fast or c2 or c3 or c4 or bench" > gpurun_out/r2j2_tests.txt 2>&1
+tail -1 gpurun_out/r2j2_tests.txt
+for i in 1 2 3; do
+ for v in cur y4z6; do FKS_LIB=build_variants/libfks_$v.so timeout 200 python tools/ab_time_raw.py 8640 3 >> gpurun_out/r2j2_ab.txt 2>&1; done
+done
+cat gpurun_out/r2j2_ab.txt
