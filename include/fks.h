@@ -193,6 +193,13 @@ fks_status fks_get_fast_layout(const fks_ctx* h, int* ctas_per_cell, int* concur
  * dirs_host [n_dirs][3] and weights w_host [n_dirs] (n_dirs = n_theta*n_phi).  Synchronous. */
 fks_status fks_get_tables(const fks_ctx* h, double* a_host, double* b_host, double* dirs_host, double* w_host);
 
+/* Test-only (no device needed): the static per-phase task schedule of the N = 16 / 24 term-loop kernel
+ * (csrc/small.cu).  Phases 0..3 = A (Z + X of y-class 2), B (Y of class 0), C (X0 + Y1), D (X1 + Y2).  Writes the
+ * warp count, the Z / Y slot counts and the X slot count per y-class, cnt[4][16] (items per warp) and
+ * items[4][16][12] (item = type << 5 | slot; type 0 = Z, 1 = Y, 2 = X).  Any out pointer may be NULL.
+ * Returns 0, or -1 for another N. */
+int fks_small_schedule(int N, int* warps, int* nzs, int* nys, int* nxs, unsigned char* cnt, unsigned char* items);
+
 /* Test-only: the per-axis whole-cell shifts delta[3][N] of the most recent transport step (host). */
 fks_status fks_get_last_shift(const fks_ctx* h, int* delta_host);
 

@@ -26,7 +26,7 @@ EXPORTS = ["fks_collision_init", "fks_collision_init_ex", "fks_collision_batch",
            "fks_get_tables", "fks_get_last_shift", "fks_profile", "fks_profile_read", "fks_debug_timestamps", "fks_launch_count",
            "fks_sync", "fks_destroy", "fks_last_error", "fks_moments", "fks_bgk_batch", "fks_bgk_step",
            "fks_transport_setup_slab", "fks_slab_halo", "fks_slab_plane_count", "fks_transport_step_slab",
-           "fks_step_slab", "fks_step_moments", "fks_step_slab_range"]
+           "fks_step_slab", "fks_step_moments", "fks_step_slab_range", "fks_small_schedule"]
 
 
 class fks_params(C.Structure):
@@ -70,6 +70,7 @@ def load_library(path: str = None):
         "fks_step_host": ([vp, vp, vp, d], i),
         "fks_moments": ([vp, vp, vp, vp, ll, vp], i),
         "fks_step_moments": ([vp, vp, vp, d, vp, vp, vp], i),
+        "fks_small_schedule": ([i, C.POINTER(i), C.POINTER(i), C.POINTER(i), C.POINTER(i), vp, vp], i),
         "fks_transport_setup_slab": ([vp, i, i, i, i, i, ll, ll], i),
         "fks_slab_halo": ([vp, C.POINTER(i)], i),
         "fks_slab_plane_count": ([vp, C.POINTER(i)], i),
@@ -165,6 +166,19 @@ def fks_step(h: int, f_in, f_out, coll_scale: float, stream=None):
 
 def fks_step_moments(h: int, f_in, f_out, coll_scale: float, U=None, W=None, stream=None):
     _check(load_library().fks_step_moments(h, _ptr(f_in), _ptr(f_out), coll_scale, _ptr(U), _ptr(W), _stream(stream)))
+
+
+def fks_small_schedule(N: int):
+    """Test-only: the small-N kernel's per-phase schedule {warps, nzs, nys, nxs, cnt[4][16], items[4][16][12]}."""
+    import numpy as np
+    w, z, y, x = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+    cnt = np.zeros((4, 16), dtype=np.uint8)
+    items = np.zeros((4, 16, 12), dtype=np.uint8)
+    rc = load_library().fks_small_schedule(N, C.byref(w), C.byref(z), C.byref(y), C.byref(x),
+                                           cnt.ctypes.data_as(C.c_void_p), items.ctypes.data_as(C.c_void_p))
+    if rc != 0:
+        raise FksError(1, f"no small-N schedule for N = {N}")
+    return {"warps": w.value, "nzs": z.value, "nys": y.value, "nxs": x.value, "cnt": cnt, "items": items}
 
 
 def fks_step_host(h: int, f_in_host, f_out_host, coll_scale: float):

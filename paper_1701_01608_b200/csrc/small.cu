@@ -19,6 +19,7 @@
 // pinned to the TMEM lane quarter that holds their G block, the other tasks fill the least-loaded warps.
 #include <algorithm>
 #include <cmath>
+#include <cstring>
 #include <vector>
 #include "fks_internal.cuh"
 
@@ -475,6 +476,26 @@ constexpr int warps_for() { return N == 16 ? 8 : 12; }
 }  // namespace sm
 
 bool small_available(const Ctx& c) { return (c.N == 16 || c.N == 24) && c.P == 3 * c.N / 2; }
+
+// Test-only (fks.h): the host-built per-phase task schedule of the small-N kernel, no device needed.
+extern "C" int fks_small_schedule(int N, int* warps, int* nzs, int* nys, int* nxs, unsigned char* cnt,
+                                  unsigned char* items) {
+  if (N != 16 && N != 24) return -1;
+  const int W = N == 16 ? sm::warps_for<16>() : sm::warps_for<24>();
+  const sm::Sched s = N == 16 ? sm::make_schedule<16>(W) : sm::make_schedule<24>(W);
+  if (warps) *warps = W;
+  if (nzs) *nzs = N == 16 ? sm::Geo<16>::NZS : sm::Geo<24>::NZS;
+  if (nys) *nys = N == 16 ? sm::Geo<16>::NYS : sm::Geo<24>::NYS;
+  if (nxs) *nxs = N == 16 ? sm::Geo<16>::NXS : sm::Geo<24>::NXS;
+  for (int ph = 0; ph < 4; ph++)  // ABI layout cnt[4][16], items[4][16][12]
+    for (int w = 0; w < 16; w++) {
+      const bool in = w < sm::kMaxWarps;
+      if (cnt) cnt[ph * 16 + w] = in ? s.cnt[ph][w] : 0;
+      for (int i = 0; i < 12; i++)
+        if (items) items[(ph * 16 + w) * 12 + i] = (in && i < sm::kMaxItems) ? s.item[ph][w][i] : 0;
+    }
+  return 0;
+}
 
 static int small_smax() { return 16; }
 

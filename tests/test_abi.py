@@ -88,3 +88,29 @@ def test_product_never_imports_oracle():
                 txt = open(os.path.join(dirpath, fn)).read()
                 assert not re.search(r"^\s*(from|import)\s+oracle", txt, re.M), fn
                 assert "fks_oracle" not in txt, fn
+
+
+@pytest.mark.parametrize("N", [16, 24])
+def test_small_schedule_host_logic(N):
+    """The small-N kernel's static schedule (built on the host, no device): every slot of every phase appears
+    exactly once; X slots run on a warp of their TMEM lane quarter (slot % 4 == warp % 4), whose G block they
+    own across terms; phase A = Z + X, B = Y, C and D = X + Y; the makespan (Z = 2 units) is within one unit of
+    the balanced bound."""
+    sc = binding.fks_small_schedule(N)
+    W, nzs, nys, nxs = sc["warps"], sc["nzs"], sc["nys"], sc["nxs"]
+    for ph in range(4):
+        seen = []
+        load = []
+        for w in range(W):
+            items = [int(x) for x in sc["items"][ph, w, :sc["cnt"][ph, w]]]
+            seen += items
+            load.append(sum(2 if it >> 5 == 0 else 1 for it in items))
+            for it in items:
+                if it >> 5 == 2:
+                    assert (it & 31) % 4 == w % 4, (ph, w, it)
+        want = ({(0 << 5) | s for s in range(nzs)} if ph == 0 else set()) | \
+               ({(1 << 5) | s for s in range(nys)} if ph != 0 else set()) | \
+               ({(2 << 5) | s for s in range(nxs)} if ph != 1 else set())
+        assert sorted(seen) == sorted(want), ph
+        assert max(load) <= -(-sum(load) // W) + 1, (ph, load)
+    assert sc["cnt"][:, W:].sum() == 0
