@@ -446,3 +446,22 @@ def test_small_path_more_units_than_ctas(cuda_device):
     idx = [0, 1, 77, 149]
     ref = oracle_Q(f[idx].cpu().numpy(), cfg_tables("c1"))
     assert rel_err_per_cell(Q[idx].cpu().numpy(), ref).max() <= TOL_Q
+
+
+@pytest.mark.parametrize("N,kernel,kw", [(32, 1, {}), (24, 2, {"vhs_alpha": 0.5}), (16, 2, {"vhs_alpha": 0.25}),
+                                         (32, 0, {"quad_rule": 1})])
+def test_fast_paths_other_kernels_and_rules(cuda_device, N, kernel, kw):
+    """Both fast paths are table-driven: Maxwell molecules on the N = 32 kernel, VHS on the small-N kernel (N = 24,
+    16) and the paper's rectangle quadrature rule on N = 32, each against the oracle (few directions and radial
+    nodes so that the oracle stays fast)."""
+    f = inputs.random_field(2, N, seed=90 + N + kernel, signed=False).to(cuda_device)
+    col = B.Collision(N, L_BOX, 4, 2, kernel, **kw)
+    assert col.info["path"] == B.FKS_PATH_FAST
+    Q = col.collision_batch(f).cpu().numpy()
+    okw = {}
+    if "vhs_alpha" in kw:
+        okw["alpha"] = kw["vhs_alpha"]
+    if "quad_rule" in kw:
+        okw["rule"] = kw["quad_rule"]
+    ref = oracle_Q(f.cpu().numpy(), oracle_tables(N, L_BOX, 4, 2, kernel, **okw))
+    assert rel_err_per_cell(Q, ref).max() <= TOL_Q
