@@ -40,7 +40,7 @@ struct Geo {
   static constexpr int SMEM = (W1_E + 2 * W2_E) * 16;
 };
 
-constexpr int kMaxWarps = 12, kMaxItems = 12;
+constexpr int kMaxWarps = 16, kMaxItems = 12;
 enum { T_Z = 0, T_Y = 1, T_X = 2 };
 // phases: 0 = A (Z + X of class 2), 1 = B (Y0), 2 = C (X0 + Y1), 3 = D (X1 + Y2)
 struct Sched {
@@ -470,8 +470,11 @@ static Sched make_schedule(int warps) {
   return s;
 }
 
+#ifndef FKS_SMALL_WARPS24
+#define FKS_SMALL_WARPS24 12
+#endif
 template <int N>
-constexpr int warps_for() { return N == 16 ? 8 : 12; }
+constexpr int warps_for() { return N == 16 ? 8 : FKS_SMALL_WARPS24; }
 
 }  // namespace sm
 
