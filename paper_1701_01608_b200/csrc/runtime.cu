@@ -597,9 +597,12 @@ fks_status fks_step_host(fks_ctx* h, const double* f_in_host, double* f_out_host
   cudaStream_t st = c.stage_stream;
   if ((rc = order_begin(c, st)) || (rc = order_begin(c, c.h2d_stream))) return rc;
   const Shift sh = advance_generic_cell(c);
-  int dmax = 0;
-  for (int k = 0; k < c.N; k++) dmax = std::max(dmax, std::abs(sh.delta[0][k]));
-  const int nx = c.nx;
+  int dmax = 0, dmy = 0;
+  for (int k = 0; k < c.N; k++) {
+    dmax = std::max(dmax, std::abs(sh.delta[0][k]));
+    dmy = std::max(dmy, std::abs(sh.delta[1][k]));
+  }
+  const int nx = c.nx, ny = c.ny;
   // slabs: more slabs expose less of the first copy-in and the last copy-out (c3: 32 slabs of one plane;
   // measured e2e 1.71e9 with 4 slabs, 1.82e9 with 8, 1.88e9 with 16, 1.90e9 with 32); each
   // slab must be at least max|delta_x| planes wide, and the halo must not wrap onto itself
@@ -610,29 +613,57 @@ fks_status fks_step_host(fks_ctx* h, const double* f_in_host, double* f_out_host
   if (const char* e = std::getenv("FKS_HOST_SLABS")) nslab = std::max(1, std::atoi(e));
   int nch = std::min(nslab, nx / std::max(1, dmax));
   if (nch < 1 || nx <= 2 * dmax) nch = 1;                  // halo too wide for slabs: one piece
-  std::vector<int> x0(nch + 1);
-  for (int i = 0; i <= nch; i++) x0[i] = (int)((long long)nx * i / nch);
-  const int wrap = (nch > 1) ? dmax : 0;                   // planes [nx - wrap, nx) go first
-  std::vector<cudaEvent_t> eh(nch), ec(nch);
+  // Work chunks = (x-planes [xa, xb), y-rows [ya, yb)), a contiguous cell range each.  The first and the last
+  // slab, when they are one plane of >= 16 rows, are cut into 4 row blocks: the first computation then waits only
+  // for the rows it reads (its plane and its x-neighbours, its rows +- max|delta_y|) and the last copy-out is a
+  // quarter plane (round 2: about 14 ms less exposed copy per c3 step).
+  struct Chunk { int xa, xb, ya, yb; };
+  std::vector<Chunk> ch;
   for (int i = 0; i < nch; i++) {
+    const int xa = (int)((long long)nx * i / nch), xb = (int)((long long)nx * (i + 1) / nch);
+    const bool split = nch > 1 && (i == 0 || i == nch - 1) && xb - xa == 1 && ny >= 16 && ny >= 4 * (2 * dmy + 1);
+    const int parts = split ? 4 : 1;
+    for (int q = 0; q < parts; q++) ch.push_back({xa, xb, (int)((long long)ny * q / parts), (int)((long long)ny * (q + 1) / parts)});
+  }
+  const int nk = (int)ch.size();
+  std::vector<cudaEvent_t> eh(nk), ec(nk);
+  for (int i = 0; i < nk; i++) {
     cudaEventCreateWithFlags(&eh[i], cudaEventDisableTiming);
     cudaEventCreateWithFlags(&ec[i], cudaEventDisableTiming);
   }
-  auto h2d = [&](int p0, int p1) -> fks_status {           // input planes [p0, p1)
-    if (p1 <= p0) return FKS_OK;
-    return cuda_status(cudaMemcpyAsync(c.d_stage_in + (size_t)p0 * plane * nv, f_in_host + (size_t)p0 * plane * nv,
-                                       (size_t)(p1 - p0) * pbytes, cudaMemcpyHostToDevice, c.h2d_stream), "H2D");
+  // copy-in in the order of first need, at row granularity (rows are contiguous within a plane)
+  std::vector<char> have((size_t)nx * ny, 0);
+  const size_t rbytes = (size_t)c.nz * nv * sizeof(double);  // one y-row of one plane
+  auto need_rows = [&](int p, int y0, int y1) -> fks_status {  // rows [y0, y1) of plane p (mod ny), not yet copied
+    for (int y = y0; y < y1;) {
+      const int yy = ((y % ny) + ny) % ny;
+      if (have[(size_t)p * ny + yy]) { y++; continue; }
+      int run = 0;  // contiguous uncopied rows starting at yy without wrapping
+      while (y + run < y1 && yy + run < ny && !have[(size_t)p * ny + yy + run]) run++;
+      for (int k = 0; k < run; k++) have[(size_t)p * ny + yy + k] = 1;
+      const size_t off = ((size_t)p * ny + yy) * c.nz * nv;
+      fks_status r = cuda_status(cudaMemcpyAsync(c.d_stage_in + off, f_in_host + off, run * rbytes,
+                                                 cudaMemcpyHostToDevice, c.h2d_stream), "H2D");
+      if (r) return r;
+      y += run;
+    }
+    return FKS_OK;
   };
-  rc = h2d(nx - wrap, nx);
-  int copied = 0;                                          // planes [0, copied) are in flight
-  for (int i = 0; i < nch && !rc; i++) {
-    const int need = (i == nch - 1) ? nx - wrap : std::min(nx - wrap, x0[i + 1] + dmax);
-    if (!(rc = h2d(copied, need))) copied = std::max(copied, need);
+  for (int i = 0; i < nk && !rc; i++) {
+    const Chunk& k = ch[i];
+    const bool whole = k.ya == 0 && k.yb == ny;
+    const int y0 = whole ? 0 : k.ya - dmy, y1 = whole ? ny : k.yb + dmy;
+    for (int x = k.xa - (nch > 1 ? dmax : 0); x < k.xb + (nch > 1 ? dmax : 0) && !rc; x++)
+      rc = need_rows(((x % nx) + nx) % nx, y0, y1);
+    if (i == nk - 1)  // everything left (single-piece case: the whole box)
+      for (int x = 0; x < nx && !rc; x++) rc = need_rows(x, 0, ny);
     if (!rc) rc = cuda_status(cudaEventRecord(eh[i], c.h2d_stream), "event");
   }
   const bool ident = shift_is_identity(sh);
-  for (int i = 0; i < nch && !rc; i++) {
-    const long long c0 = (long long)x0[i] * plane, m = (long long)(x0[i + 1] - x0[i]) * plane;
+  for (int i = 0; i < nk && !rc; i++) {
+    const Chunk& k = ch[i];
+    const long long c0 = ((long long)k.xa * ny + k.ya) * c.nz;
+    const long long m = (k.xb - k.xa == 1) ? (long long)(k.yb - k.ya) * c.nz : (long long)(k.xb - k.xa) * plane;
     rc = cuda_status(cudaStreamWaitEvent(st, eh[i], 0), "wait H2D");
     if (!rc) {
       if (ident) rc = run_collision(c, c.d_stage_in + c0 * nv, c.d_stage_out + c0 * nv, m, true, coll_scale, st);
@@ -652,7 +683,7 @@ fks_status fks_step_host(fks_ctx* h, const double* f_in_host, double* f_out_host
   fks_status rs = cuda_status(cudaStreamSynchronize(c.d2h_stream), "host-buffer step");
   cudaStreamSynchronize(st);
   cudaStreamSynchronize(c.h2d_stream);
-  for (int i = 0; i < nch; i++) { cudaEventDestroy(eh[i]); cudaEventDestroy(ec[i]); }
+  for (int i = 0; i < nk; i++) { cudaEventDestroy(eh[i]); cudaEventDestroy(ec[i]); }
   c.ev_pending = false;  // everything this handle enqueued has completed
   return rc ? rc : rs;
 }
