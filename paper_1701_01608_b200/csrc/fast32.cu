@@ -28,23 +28,22 @@ __device__ __forceinline__ void mbar_expect(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(bar)),
                "r"(bytes) : "memory");
 }
-// Waiting warps are suspended by the hardware (try_wait with a suspend-time hint) instead of spinning: spinning
-// waiters cost ~14 % of the issue slots of the working warps sharing their sub-partition (ncu, hot kernel v4).
-// Waiting warps back off exponentially (test_wait + nanosleep 32 ns .. 1 us): spinning waiters issued ~35 % of
-// all instructions of the 16-warp term-loop kernel (ncu) and took issue slots from the working warps.
+// Waiting warps are suspended by the hardware (try_wait with a suspend-time hint) until the phase completes: a
+// back-off with __nanosleep over-slept by up to its last interval on every hand-off of the term loop's chains.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t a = (uint32_t)__cvta_generic_to_shared(bar);
   uint32_t done = 0;
-  unsigned ns = 32;
   unsigned spins = 0;
   while (true) {
-    asm volatile("{ .reg .pred p; mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-                 : "=r"(done) : "r"(a), "r"(parity) : "memory");
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(done) : "r"(a), "r"(parity), "r"(20000u) : "memory");
     if (done) break;
-    __nanosleep(ns);
-    if (ns < 1024) ns <<= 1;
-    if (++spins > (1u << 24)) asm volatile("trap;");  // never hang the GPU on a byte-count bug
+    if (++spins > (1u << 20)) asm volatile("trap;");  // never hang the GPU on a byte-count bug
   }
+}
+// arrive (release, CTA scope) on a barrier initialised with count 1
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"((uint32_t)__cvta_generic_to_shared(bar)) : "memory");
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
@@ -116,18 +115,29 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+#ifndef FKS_POLL_NS
+#define FKS_POLL_NS 2048
+#endif
+// Team counters are polled with relaxed loads and acquired once when the target is seen: an acquire load at GPU
+// scope compiles to LDG.STRONG.GPU + CCTL.IVALL, and invalidating the SM's L1 on every poll iteration evicted the
+// other warps' cached table loads and spill lines.  The interval is long (2 us): the waits are rare, and a shorter
+// interval measured slower (acquire polling: 128 ns 122.2 ms, 2 us 120.0 ms; relaxed: 128 ns 121.1, 512 ns 119.8,
+// 2 us 119.1 ms per 8640-cell c3 collision).
 __device__ __forceinline__ void poll_ge(const unsigned* p, unsigned target) {
   unsigned spins = 0;
-  while (ld_acquire(p) < target) {
-    __nanosleep(128);
+  while (ld_relaxed(p) < target) {
+    __nanosleep(FKS_POLL_NS);
     if (++spins > (1u << 25)) asm volatile("trap;");  // never hang the GPU on a counting bug
   }
+  (void)ld_acquire(p);
 }
-// publication of W1 by one thread after a named barrier: release semantics are cumulative over the stores the
-// barrier made visible to it (a separate fence.sc cost ~1.3 K cycles per term)
-__device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
-  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
+// Counter updates use fence.sc + atomicAdd: red.release.gpu (MEMBAR.ALL.GPU + RED) measured 4 % slower on the
+// c3 collision (124.3 vs 119.1 ms per 8640 cells, profiles/r02_experiments.txt).
 __device__ __forceinline__ int vload(const int* p) { return *reinterpret_cast<const volatile int*>(p); }
 __device__ __forceinline__ void nbar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
@@ -162,9 +172,15 @@ struct InK {
 };
 
 // Pruned inverse transform of one output class r (runtime, warp-uniform): z(3q + r) = sum_{l=-15..15} Z(l)
-// e^{2 pi i l (3q + r)/48}, inputs Z(l) at base[(l + 15) * ld].  Radix-3 combine (only l mod 48 in 0..15 and
-// 33..47 are present) + FFT16; z(3q + r) ends in u[qslot(q)].  ONE instance per warp role keeps the kernel's hot
-// code inside the instruction cache (templated per-class copies thrashed it: ncu no_instruction stalls).
+// e^{2 pi i l (3q + r)/48}, inputs Z(l) at base[(l + 15) * ld].  Two forms (fft_dev.cuh):
+//   xform48     radix-3 DIF combine (only l mod 48 in 0..15 and 33..47 are present) with the twiddles w48^{rm},
+//               then FFT16; z(3q + r) ends in u[qslot(q)].  Used by the Y warps (and, inlined, the X warps).
+//   xform48_gt  Good-Thomas form: no inter-stage twiddles, the 16-point stage in tangent form (-16 % FP64
+//               instructions); slot k2 ends in u[qslot(k2)] and holds z(3 pfa_q(r, k2) + r).  Used by the Z warps,
+//               whose outputs go to "virtual" W1 planes v = 16 r + k2 (pz = pfa_p(v), mapped back at the G
+//               write-out).  In the Y and X roles the same form measured slower (profiles/r02_experiments.txt).
+// ONE instance per warp role keeps the kernel's hot code inside the instruction cache (templated per-class copies
+// thrashed it: ncu no_instruction stalls).
 __device__ __forceinline__ void xform48(const double2* base, int ld, int r, double2 (&u)[16]) {
   u[0] = base[15 * ld];
   if (r == 0) {
@@ -187,6 +203,20 @@ __device__ __forceinline__ void xform48(const double2* base, int ld, int r, doub
   }
   fftd::fft16<1>(u);
 }
+__device__ __forceinline__ void xform48_gt(const double2* base, int ld, int r, double2 (&u)[16]) {
+  u[0] = base[15 * ld];
+  if (r == 0) {
+#pragma unroll
+    for (int m = 1; m < 16; m++) u[fftd::pfa_n2(m)] = fftd::cadd(base[(m + 15) * ld], base[(m - 1) * ld]);
+  } else {
+    const double sg = (r == 1) ? 0.86602540378443864676 : -0.86602540378443864676;
+#pragma unroll
+    for (int m = 1; m < 16; m++) u[fftd::pfa_n2(m)] = fftd::pfa_combine(m, base[(m + 15) * ld], base[(m - 1) * ld], sg);
+  }
+  fftd::fft16i(u);
+}
+// transform index p of the Good-Thomas slot k2 of class r, v = 16 r + k2 (the Z warps' virtual W1 plane v)
+__device__ __forceinline__ int pfa_p(int v) { return 3 * fftd::pfa_q(v >> 4, v & 15) + (v >> 4); }
 
 __device__ __forceinline__ void tmem_ld16_async(uint32_t addr, uint32_t (&v)[16]) {
   asm volatile(
@@ -214,9 +244,10 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ uint32_t tmem_base_sh;
   __shared__ __align__(8) uint64_t bar_w1[2];
+  __shared__ __align__(8) uint64_t bar_full[2][3], bar_empty[2][3];  // Y(g,c) -> X(g,c) slot hand-offs
   __shared__ __align__(8) uint64_t bar_tab, bar_fh;
   // YX groups: per-group completion counters (Y -> X per class, X -> Y slot release)
-  __shared__ int s_yc[2][3], s_xc[2][3], s_yall[2], s_w1iss[2];
+  __shared__ int s_yall[2], s_w1iss[2];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int team = blockIdx.x / TM, k = blockIdx.x - (blockIdx.x / TM) * TM;
   constexpr int NLOW = NPEN / 2 + 1;
@@ -240,9 +271,9 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
   if (tid == 0) {
     mbar_init(&bar_w1[0]);
     mbar_init(&bar_w1[1]);
+    for (int i = 0; i < 6; i++) { mbar_init(&bar_full[0][0] + i); mbar_init(&bar_empty[0][0] + i); }
     mbar_init(&bar_tab);
     mbar_init(&bar_fh);
-    for (int i = 0; i < 6; i++) { (&s_yc[0][0])[i] = 0; (&s_xc[0][0])[i] = 0; }
     s_yall[0] = s_yall[1] = 0;
     s_w1iss[0] = s_w1iss[1] = 0;
   }
@@ -271,20 +302,6 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
     const uint32_t tX = tbase + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(warp >= 4 && warp < 6 ? 224 : 0);
     const uint32_t tPark = tX + 96u;
     const int xp = lane >> 4, xq = lane & 15;
-    int* yc = s_yc[g];
-    int* xc = s_xc[g];
-    auto wait_ge = [&](const int* ptr, int target) {
-      if (lane == 0) {
-        unsigned spins = 0;
-        unsigned ns = 32;
-        while (vload(ptr) < target) {
-          __nanosleep(ns);
-          if (ns < 512) ns <<= 1;
-          if (++spins > (1u << 26)) asm volatile("trap;");
-        }
-      }
-      __syncwarp();
-    };
     auto issue_w1 = [&](int tgi) {
       const double2* src = W1t + (tgi % NB) * (long long)W1_BUF + pz0 * NPEN;
       asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -294,18 +311,19 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
       bulk_g2s(in1, src + NPEN, W1IN_B, &bar_w1[g]);
     };
     auto try_issue_w1 = [&](int tz, bool block) {  // lane 0: bulk-copy W1(tz) once per group
+      const int sl = g;
       if (tz >= total_tg) return;
-      if (vload(&s_w1iss[g]) > tz) return;
-      if (vload(&s_yall[g]) < 3 * tz) {
+      if (vload(&s_w1iss[sl]) > tz) return;
+      if (vload(&s_yall[sl]) < 3 * tz) {
         if (!block) return;
         unsigned spins = 0;
-        while (vload(&s_yall[g]) < 3 * tz) { __nanosleep(64); if (++spins > (1u << 26)) asm volatile("trap;"); }
+        while (vload(&s_yall[sl]) < 3 * tz) { __nanosleep(64); if (++spins > (1u << 26)) asm volatile("trap;"); }
       }
       unsigned* zc = zcnt + 32 * (tz % NB);
       const unsigned target = (unsigned)(TM * (tz / NB + 1));
       if (block) poll_ge(zc, target);
-      else if (ld_acquire(zc) < target) return;
-      if (atomicCAS(&s_w1iss[g], tz, tz + 1) == tz) issue_w1(tz);
+      else if (ld_relaxed(zc) < target || ld_acquire(zc) < target) return;
+      if (atomicCAS(&s_w1iss[sl], tz, tz + 1) == tz) issue_w1(tz);
     };
     uint32_t par = 0;
     int tg = 0;
@@ -315,8 +333,8 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
       for (int t = 0; t < A.T1; t++, tg++) {
         const int T = tg;
 #ifdef FKS_V4_PHASE_TIMING  // tools/phase_timing_v4.py: an instrumented build variant only
-        long long* st = (A.dbg && lane == 0 && warp == 6 && cell == team && t >= 2 && t < 6)
-                            ? A.dbg + (long long)blockIdx.x * 128 + (t - 2) * 16 : nullptr;
+        long long* st = (A.dbg && lane == 0 && (warp == 6 || warp == 0) && cell == team && t >= 2 && t < 6)
+                            ? A.dbg + (long long)blockIdx.x * 128 + (t - 2) * 16 + (warp == 0 ? 3 : 0) : nullptr;
 #endif
         STAMP(0);
         if (!isx) {
@@ -328,11 +346,13 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
             atomicAdd(ycnt + 32 * (tg % NB), 1u);  // this group has consumed W1(tg)
           }
           STAMP(1);
-          wait_ge(&xc[c], T);  // slot c: X(g, c) of term t-1 has parked its rows
 #pragma unroll 1
           for (int pl = 0; pl < 2; pl++) {
             double2 u[16];
             xform48((pl ? in1 : in0) + (lane < K ? lane : K - 1) * K, 1, c, u);
+            // slot c is free once X(g, c) has parked the rows of term t - 1 (waited after the first transform, so
+            // that the park overlaps it)
+            if (pl == 0 && T > 0) mbar_wait(&bar_empty[g][c], (T - 1) & 1);
             if (lane < K) {
               double2* ydst = ybuf(pl, c) + lane;
 #pragma unroll
@@ -341,14 +361,14 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
           }
           __syncwarp();
           if (lane == 0) {
-            __threadfence_block();
-            atomicAdd(&yc[c], 1);
+            mbar_arrive(&bar_full[g][c]);
             if (atomicAdd(&s_yall[g], 1) + 1 == 3 * (T + 1)) try_issue_w1(tg + 1, false);  // prefetch
           }
           STAMP(2);
         } else {
           // ---------------- X warp ----------------
-          wait_ge(&yc[c], T + 1);
+          mbar_wait(&bar_full[g][c], T & 1);
+          STAMP(1);
           if (t == 0) {  // first term of the cell: zero the three G blocks
             uint32_t zw[32];
 #pragma unroll
@@ -375,16 +395,14 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
           }
           __syncwarp();
-          if (lane == 0) {
-            __threadfence_block();
-            atomicAdd(&xc[c], 1);  // the Y slot may be refilled
-          }
+          if (lane == 0) mbar_arrive(&bar_empty[g][c]);  // the Y slot may be refilled
+          STAMP(2);
 #pragma unroll 1
           for (int rx = 0; rx < 3; rx++) {
             double2 u[16];
             const double sg = (rx == 1) ? -0.86602540378443864676 : 0.86602540378443864676;
 #pragma unroll
-            for (int mm = 0; mm < 4; mm++) {  // x[4mm..4mm+3] (a) and x[16+4mm..19+4mm] (b) -> u[4mm+1..4mm+4]
+            for (int mm = 0; mm < 4; mm++) {
               uint32_t wa[16], wb[16];
               tmem_ld16_async(tPark + 16u * mm, wa);
               tmem_ld16_async(tPark + 64u + 16u * mm, wb);
@@ -394,7 +412,7 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
                 const int m = 4 * mm + k2 + 1;
                 const double2 va = make_double2(__hiloint2double((int)wa[4 * k2 + 1], (int)wa[4 * k2]),
                                                 __hiloint2double((int)wa[4 * k2 + 3], (int)wa[4 * k2 + 2]));
-                if (mm == 3 && k2 == 3) { u[0] = va; continue; }  // x[15]
+                if (mm == 3 && k2 == 3) { u[0] = va; continue; }
                 const double2 vb = make_double2(__hiloint2double((int)wb[4 * k2 + 1], (int)wb[4 * k2]),
                                                 __hiloint2double((int)wb[4 * k2 + 3], (int)wb[4 * k2 + 2]));
                 if (rx == 0) {
@@ -413,16 +431,19 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
             g_accumulate(tX + 32u * rx, u);
           }
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-          if (t == A.T1 - 1) {  // G[cell][px = 3q' + rx][pz / 2][py = 3 xq + c][pz % 2]: z-rows interleaved in pairs
-            const int pz = pz0 + xp;
-            double* Gc = A.G + cell * (long long)(P * P * P) + (long long)(pz >> 1) * (2 * P) + (pz & 1);
+          STAMP(3);
+          if (t == A.T1 - 1) {  // G[cell][px = 3q' + rx][pz / 2][py = 3 xq + c][pz % 2]: z-rows interleaved in
+                                // pairs; the virtual plane pz0 + xp holds pz = pfa_p(pz0 + xp)
+            const int pz = pfa_p(pz0 + xp);
+            const int py = 3 * xq + c;
+            double* Gc = A.G + cell * (long long)(P * P * P) + (long long)(pz >> 1) * (2 * P) + (pz & 1) + 2 * py;
 #pragma unroll 1
             for (int rx = 0; rx < 3; rx++) {
               uint32_t gw[32];
               tmem_ld32(tX + 32u * rx, gw);
 #pragma unroll
               for (int q = 0; q < 16; q++)
-                Gc[(long long)(3 * q + rx) * P * P + 2 * (3 * xq + c)] = __hiloint2double((int)gw[2 * q + 1], (int)gw[2 * q]);
+                Gc[(long long)(3 * q + rx) * P * P] = __hiloint2double((int)gw[2 * q + 1], (int)gw[2 * q]);
             }
           }
         }
@@ -523,11 +544,11 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
             const bool mir = j >= nh;
             const int jj = mir ? j - nh : j;
             double2 u[16];
-            xform48((mir ? zm : zp) + jj, nh, r, u);
+            xform48_gt((mir ? zm : zp) + jj, nh, r, u);
             if (act) {
               const int pp = mir ? (NPEN - 1) - (h0 + jj) : h0 + jj;
 #pragma unroll
-              for (int q = 0; q < 16; q++) W1b[(3 * q + r) * NPEN + pp] = u[fftd::qslot(q)];
+              for (int q = 0; q < 16; q++) W1b[(16 * r + q) * NPEN + pp] = u[fftd::qslot(q)];  // virtual plane
             }
           }
         }

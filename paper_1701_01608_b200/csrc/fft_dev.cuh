@@ -83,6 +83,71 @@ __device__ __forceinline__ void fft16(double2 (&u)[16]) {
   for (int q1 = 0; q1 < 4; q1++) bfly4<S>(u[4 * q1], u[4 * q1 + 1], u[4 * q1 + 2], u[4 * q1 + 3]);
 }
 
+// Inverse (S = +1) 16-point DFT, same contract as fft16<1>, with the second stage's twiddles folded into its
+// butterflies: w16^1 = C(1 + i t), w16^3 = C(t + i), w16^2 = h(1 + i), w16^6 = h(-1 + i), w16^9 = -C(1 + i t)
+// (C = cos pi/8, t = tan pi/8, h = 1/sqrt 2), so each radix-4 butterfly of the second stage forms its rotated
+// pair sums with DADD/DFMA and applies C or h inside the output FMAs: 144 FP64 instructions instead of 160.
+__device__ __forceinline__ void fft16i(double2 (&u)[16]) {
+  constexpr double h = 0.70710678118654752440, C = 0.92387953251128675613, t = 0.41421356237309504880;
+#pragma unroll
+  for (int m2 = 0; m2 < 4; m2++) bfly4<1>(u[m2], u[m2 + 4], u[m2 + 8], u[m2 + 12]);
+  bfly4<1>(u[0], u[1], u[2], u[3]);
+  {  // q1 = 1: twiddles 1, w, w^2, w^3
+    const double2 x0 = u[4], x1 = u[5], x2 = u[6], x3 = u[7];
+    const double ex = x2.x - x2.y, ey = x2.x + x2.y;
+    const double ax = fma(h, ex, x0.x), ay = fma(h, ey, x0.y), bx = fma(-h, ex, x0.x), by = fma(-h, ey, x0.y);
+    const double A = x1.x - x3.y, B = x1.x + x3.y, Cc = x1.y + x3.x, D = x1.y - x3.x;
+    const double cx = fma(-t, D, A), cy = fma(t, B, Cc), dx = fma(-t, Cc, B), dy = fma(t, A, D);
+    u[4] = make_double2(fma(C, cx, ax), fma(C, cy, ay));
+    u[6] = make_double2(fma(-C, cx, ax), fma(-C, cy, ay));
+    u[5] = make_double2(fma(-C, dy, bx), fma(C, dx, by));
+    u[7] = make_double2(fma(C, dy, bx), fma(-C, dx, by));
+  }
+  {  // q1 = 2: twiddles 1, w^2, w^4 = i, w^6
+    const double2 x0 = u[8], x1 = u[9], x2 = u[10], x3 = u[11];
+    const double ax = x0.x - x2.y, ay = x0.y + x2.x, bx = x0.x + x2.y, by = x0.y - x2.x;
+    const double px = x1.x - x3.x, py = x1.y - x3.y, sx = x1.x + x3.x, sy = x1.y + x3.y;
+    const double cx = px - sy, cy = py + sx, dx = sx - py, dy = sy + px;
+    u[8] = make_double2(fma(h, cx, ax), fma(h, cy, ay));
+    u[10] = make_double2(fma(-h, cx, ax), fma(-h, cy, ay));
+    u[9] = make_double2(fma(-h, dy, bx), fma(h, dx, by));
+    u[11] = make_double2(fma(h, dy, bx), fma(-h, dx, by));
+  }
+  {  // q1 = 3: twiddles 1, w^3, w^6, w^9
+    const double2 x0 = u[12], x1 = u[13], x2 = u[14], x3 = u[15];
+    const double e1 = x2.x + x2.y, e2 = x2.x - x2.y;
+    const double ax = fma(-h, e1, x0.x), ay = fma(h, e2, x0.y), bx = fma(h, e1, x0.x), by = fma(-h, e2, x0.y);
+    const double A = x1.x - x3.y, B = x1.x + x3.y, Cc = x1.y + x3.x, D = x1.y - x3.x;
+    const double cx = fma(t, B, -Cc), cy = fma(t, D, A), dx = fma(t, A, -D), dy = fma(t, Cc, B);
+    u[12] = make_double2(fma(C, cx, ax), fma(C, cy, ay));
+    u[14] = make_double2(fma(-C, cx, ax), fma(-C, cy, ay));
+    u[13] = make_double2(fma(-C, dy, bx), fma(C, dx, by));
+    u[15] = make_double2(fma(C, dy, bx), fma(-C, dx, by));
+  }
+}
+
+// Good-Thomas (prime-factor) form of the pruned inverse length-48 transform, 48 = 3 x 16 coprime: with the input
+// map n = (16 n1 + 3 n2) mod 48 and the output map k = (16 k1 + 33 k2) mod 48, e^{2 pi i n k/48} =
+// w3^{n1 k1} w16^{n2 k2}: a 3-point DFT over n1 and a 16-point DFT over n2, no inter-stage twiddles.  For the
+// retained modes l = -15..15 (transform index l mod 48; 16..32 absent) the group of n2 holds Z(m) and Z(m - 16),
+// m = 3 n2 mod 16, and its class-r value is  w3^{-r j} (Z(m) + w3^{2r} Z(m - 16)),  j = 3 n2 div 16; the 16-point
+// transform then leaves z(k) at slot k2 with k = 3 pfa_q(r, k2) + r.
+__host__ __device__ __forceinline__ constexpr int pfa_q(int r, int k2) { return (5 * r + 11 * k2) & 15; }
+__host__ __device__ __forceinline__ constexpr int pfa_n2(int m) { return (11 * m) & 15; }  // m = 3 n2 mod 16
+// u[pfa_n2(m)] from a = Z(m), v = Z(m - 16), m = 1..15; r != 0 with sg = +sin(2pi/3) (r = 1) or - (r = 2)
+// (m is a constant after unrolling, so the branch folds)
+__device__ __forceinline__ double2 pfa_combine(int m, double2 a, double2 v, double sg) {
+  const int j = (3 * pfa_n2(m)) >> 4;
+  if (j == 0) {  // a + w v, w = w3^{2r} = (-1/2, -sg)
+    return make_double2(fma(sg, v.y, fma(-0.5, v.x, a.x)), fma(-sg, v.x, fma(-0.5, v.y, a.y)));
+  } else if (j == 2) {  // conj(w) a + v
+    return make_double2(fma(-sg, a.y, fma(-0.5, a.x, v.x)), fma(sg, a.x, fma(-0.5, a.y, v.y)));
+  } else {  // w a + conj(w) v
+    const double sx = a.x + v.x, sy = a.y + v.y, dx = a.x - v.x, dy = a.y - v.y;
+    return make_double2(fma(-0.5, sx, sg * dy), fma(-0.5, sy, -sg * dx));
+  }
+}
+
 // Radix-R combine of class r:  u[m] = w_n^{S r m} sum_j x[m + 16 j] w_R^{S j r},  n = 16 R.
 // `in.nz(i)` (a compile-time constant after unrolling) marks structurally non-zero inputs; `in(i)` reads one.
 template <int R, int S, int r, class In>

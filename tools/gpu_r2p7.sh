@@ -1,0 +1,9 @@
+# next-term table loads held in registers across the Z class tasks (zpf*) vs mbwZ
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+FKS_LIB=build_variants/libfks_ptzpfZ.so timeout 200 python tools/phase_timing_v4.py c3 1440 > gpurun_out/r2p7_phase.txt 2>&1
+cat gpurun_out/r2p7_phase.txt
+for i in 1 2; do
+ for v in mbwZ zpfZ zpf; do FKS_LIB=build_variants/libfks_$v.so timeout 200 python tools/ab_time_raw.py 8640 3 >> gpurun_out/r2p7_ab.txt 2>&1; done
+done
+cat gpurun_out/r2p7_ab.txt

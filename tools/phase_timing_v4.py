@@ -24,10 +24,12 @@ raw = buf[: 144 * 128].reshape(144, 8, 16)[:, :4, :]  # [cta][term][slot]
 raw = raw[raw[:, 0, 0] > 0]
 yx, z = raw[:, :, :8].astype(float), raw[:, :, 8:].astype(float)
 print("CTAs sampled:", len(raw))
-for name, a, b in [("YX: wait W1 (poll + TMA)", 0, 1), ("YX: R1 (Y0,Y0,Y1)", 1, 2), ("YX: R2 (X c=0)", 2, 3),
-                   ("YX: R3 (Y1,Y2,Y2)", 3, 4), ("YX: R4+R5 (X c=1,2)", 4, 5)]:
+for name, a, b in [("Y: wait W1 (poll + TMA)", 0, 1), ("Y: slot wait + 2 tasks", 1, 2),
+                   ("X: wait Y", 3, 4), ("X: park", 4, 5), ("X: 3 tasks", 5, 6)]:
     d = yx[:, :, b] - yx[:, :, a]
     print(f"{name:28s} median {np.median(d):8.0f}  p10 {np.percentile(d, 10):8.0f}  p90 {np.percentile(d, 90):8.0f}")
+d = yx[:, 1:, 3] - yx[:, :-1, 3]
+print(f"{'X term period':28s} median {np.median(d):8.0f}")
 d = yx[:, 1:, 0] - yx[:, :-1, 0]
 print(f"{'YX term period':28s} median {np.median(d):8.0f}")
 for name, a, b in [("Z: wait tab", 0, 1), ("Z: products", 1, 2), ("Z: wait W1 buffer free", 2, 3),
