@@ -333,7 +333,7 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
       for (int t = 0; t < A.T1; t++, tg++) {
         const int T = tg;
 #ifdef FKS_V4_PHASE_TIMING  // tools/phase_timing_v4.py: an instrumented build variant only
-        long long* st = (A.dbg && lane == 0 && (warp == 6 || warp == 0) && cell == team && t >= 2 && t < 6)
+        long long* st = (A.dbg && lane == 0 && (warp == 6 || warp == 0) && cell == team + 2 * A.nteams && t >= 2 && t < 6)
                             ? A.dbg + (long long)blockIdx.x * 128 + (t - 2) * 16 + (warp == 0 ? 3 : 0) : nullptr;
 #endif
         STAMP(0);
@@ -443,7 +443,8 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
               tmem_ld32(tX + 32u * rx, gw);
 #pragma unroll
               for (int q = 0; q < 16; q++)
-                Gc[(long long)(3 * q + rx) * P * P] = __hiloint2double((int)gw[2 * q + 1], (int)gw[2 * q]);
+                Gc[(long long)(3 * q + rx) * P * P] =
+                    __hiloint2double((int)gw[2 * q + 1], (int)gw[2 * q]);
             }
           }
         }
@@ -473,31 +474,39 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
       for (int t = 0; t < A.T1; t++, tg++) {
         const double2* tb = A.tabT + (long long)t * LHN + K * h0;     // the member's table block (L2)
 #ifdef FKS_V4_PHASE_TIMING
-        long long* st = (A.dbg && zt == 0 && cell == team && t >= 2 && t < 6)
+        long long* st = (A.dbg && zt == 0 && cell == team + 2 * A.nteams && t >= 2 && t < 6)
                             ? A.dbg + (long long)blockIdx.x * 128 + (t - 2) * 16 + 8 : nullptr;
 #endif
         STAMP(0);
-        STAMP(1);
-        // products: Z = (a + ib) f^ for the staged pencils, and for their mirrors (-lx,-ly): (a + ib) conj(f^)
-        // at the reversed lz (a, b even; f real)
-        {  // element pairs {i, 30 - i} of pencil j, e = i * nh + j; i = e / nh by multiply-high (exact: e nh < 2^32).
-           // Four iterations are loaded before any store (the product buffers never alias the staged inputs).
+        // Warp 12 publishes W1(tg - 1) (fence + team counter) and waits for the buffer of W1(tg) to be free while
+        // warps 13-15 form the products, so neither the store drain nor the poll sits on the Z warps' chain.
+        if (zt < 32) {
+          if (zt == 0) {
+            if (tg >= 1) {
+              __threadfence();
+              atomicAdd(zcnt + 32 * ((tg - 1) % NB), 1u);
+            }
+            if (tg >= NB) poll_ge(ycnt + 32 * (tg % NB), (unsigned)(2 * TM * (tg / NB)));  // buffer free
+          }
+          __syncwarp();
+        } else {
+          // products: Z = (a + ib) f^ for the staged pencils, and for their mirrors (-lx,-ly): (a + ib) conj(f^)
+          // at the reversed lz (a, b even; f real).  Element pairs {i, 30 - i} of pencil j, e = i * nh + j; i = e / nh
+          // by multiply-high (exact: e nh < 2^32); every table load of a thread is issued before the first product
+          constexpr int NPT = NZT - 32;                       // product threads
+          constexpr int ZIT = (16 * MAXH + NPT - 1) / NPT;
+          const int zq = zt - 32;
           const unsigned mdiv = 0xffffffffu / (unsigned)nh + 1u;
           const double2* __restrict__ fr = fh;  // f^ block in shared memory
           const double2* __restrict__ tr = tb;
           double2* __restrict__ pw = zp;
           double2* __restrict__ mw = zm;
           const int ne = 16 * nh;
-          // every load of this thread (<= ZIT iterations) is issued before the first product: one L2 round trip
-          constexpr int ZIT = (16 * MAXH + NZT - 1) / NZT;  // all table loads of this thread in one L2 round
-#pragma unroll 1
-          for (int zb = 0; zb * ZIT * NZT < ne; zb++) {
-          const int zt0 = zt + zb * ZIT * NZT;
           double2 f1[ZIT], a1[ZIT], f2[ZIT], a2[ZIT];
           int o1[ZIT], o2[ZIT];
 #pragma unroll
           for (int u = 0; u < ZIT; u++) {
-            const int e = min(zt0 + u * NZT, ne - 1);
+            const int e = min(zq + u * NPT, ne - 1);
             const int i = (int)__umulhi((unsigned)e, mdiv), j = e - i * nh;
             o1[u] = i * nh + j;
             o2[u] = (30 - i) * nh + j;
@@ -508,29 +517,18 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
           for (int u = 0; u < ZIT; u++) {
             f1[u] = fr[o1[u]];  // shared memory
             f2[u] = fr[o2[u]];
-            if (zt0 + u * NZT < ne) {
+            if (zq + u * NPT < ne) {
               pw[o1[u]] = make_double2(fma(a1[u].x, f1[u].x, -a1[u].y * f1[u].y), fma(a1[u].x, f1[u].y, a1[u].y * f1[u].x));
               pw[o2[u]] = make_double2(fma(a2[u].x, f2[u].x, -a2[u].y * f2[u].y), fma(a2[u].x, f2[u].y, a2[u].y * f2[u].x));
               mw[o1[u]] = make_double2(fma(a2[u].x, f2[u].x, a2[u].y * f2[u].y), fma(-a2[u].x, f2[u].y, a2[u].y * f2[u].x));
               mw[o2[u]] = make_double2(fma(a1[u].x, f1[u].x, a1[u].y * f1[u].y), fma(-a1[u].x, f1[u].y, a1[u].y * f1[u].x));
             }
           }
-          }
         }
-        nbar(3, NZT);  // products complete (after the cell's last term the f^ block is free)
+        STAMP(1);
+        nbar(3, NZT);  // products complete, W1(tg - 1) published, W1(tg)'s buffer free
         if (zt == 0 && t == A.T1 - 1 && cell + A.nteams < ncells) issue_fh(cell + A.nteams);
-        // publish W1(tg - 2) and W1(tg - 1) every second term: one store drain per pair (it costs ~1.4 K cycles
-        // on the Z warps, which set the period; the consumers have slack)
-        if (zt == 0 && tg >= 2 && (tg & 1) == 0) {
-          __threadfence();
-          atomicAdd(zcnt + 32 * ((tg - 2) % NB), 1u);
-          atomicAdd(zcnt + 32 * ((tg - 1) % NB), 1u);
-        }
         STAMP(2);
-        if (zt == 0) {
-          if (tg >= NB) poll_ge(ycnt + 32 * (tg % NB), (unsigned)(2 * TM * (tg / NB)));  // buffer free
-        }
-        nbar(3, NZT);
         STAMP(3);
         double2* W1b = W1t + (tg % NB) * (long long)W1_BUF;
         {  // 4 Z warps: single class tasks tau = r * na + j, 2 rounds of 128 threads cover 3 na <= 246
@@ -556,9 +554,8 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
         STAMP(4);
       }
     }
-    if (zt == 0 && tg > 0) {  // publish what is left (tg even: W1(tg-2), W1(tg-1); tg odd: W1(tg-1))
+    if (zt == 0 && tg > 0) {  // publish the last term
       __threadfence();
-      if ((tg & 1) == 0 && tg >= 2) atomicAdd(zcnt + 32 * ((tg - 2) % NB), 1u);
       atomicAdd(zcnt + 32 * ((tg - 1) % NB), 1u);
     }
   }

@@ -1,7 +1,7 @@
-set -x
+# Good-Thomas transform in the Y / X roles again, now with mbarrier hand-offs and relaxed polls
 cd $GRAFT_REPO_ROOT
-FKS_LIB=build_variants/libfks_yprod.so timeout 300 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "fast_path_vs_oracle or random_and_ragged" > gpurun_out/r2q2_tests.txt 2>&1
-tail -3 gpurun_out/r2q2_tests.txt
+mkdir -p gpurun_out
 for i in 1 2; do
- for v in cur yprod; do FKS_LIB=build_variants/libfks_$v.so timeout 120 python tools/ab_time_raw.py 8640 3 2>&1 | tail -1; done
+ for v in cur ygt xgt yxgt; do FKS_LIB=build_variants/libfks_$v.so timeout 200 python tools/ab_time_raw.py 8640 3 >> gpurun_out/r2q2_ab.txt 2>&1; done
 done
+cat gpurun_out/r2q2_ab.txt

@@ -32,7 +32,7 @@ d = yx[:, 1:, 3] - yx[:, :-1, 3]
 print(f"{'X term period':28s} median {np.median(d):8.0f}")
 d = yx[:, 1:, 0] - yx[:, :-1, 0]
 print(f"{'YX term period':28s} median {np.median(d):8.0f}")
-for name, a, b in [("Z: wait tab", 0, 1), ("Z: products", 1, 2), ("Z: wait W1 buffer free", 2, 3),
+for name, a, b in [("Z: products (zt 0)", 0, 1), ("Z: barrier + publish", 1, 2), ("Z: wait W1 buffer free", 2, 3),
                    ("Z: class tasks + stores", 3, 4)]:
     d = z[:, :, b] - z[:, :, a]
     print(f"{name:28s} median {np.median(d):8.0f}  p10 {np.percentile(d, 10):8.0f}  p90 {np.percentile(d, 90):8.0f}")
