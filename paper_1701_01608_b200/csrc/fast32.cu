@@ -104,10 +104,18 @@ struct Args {
   long long* dbg;        // optional per-phase clock64 stamps (tools/phase_timing.py); nullptr in production
 };
 
+// Phase accounting (instrumented build variant only, tools/phase_timing_v4.py): lane 0 of the sampled warps adds
+// the clock64 time of each phase of every term of one steady-state cell (the third of its team) into pt_acc[i] and
+// writes the sums when that cell is done.
 #ifdef FKS_V4_PHASE_TIMING
-#define STAMP(i) do { if (st) st[i] = clock64(); } while (0)
+#define PT_DECL long long pt_acc[6] = {0, 0, 0, 0, 0, 0}; long long pt_last = clock64();
+#define PT(i) do { const long long pt_n = clock64(); pt_acc[i] += pt_n - pt_last; pt_last = pt_n; } while (0)
+#define PT_FLUSH(sel, off) do { if ((sel) && A.dbg) for (int pt_i = 0; pt_i < 6; pt_i++) \
+    A.dbg[(long long)blockIdx.x * 128 + (off) + pt_i] = pt_acc[pt_i]; } while (0)
 #else
-#define STAMP(i) do { } while (0)
+#define PT_DECL
+#define PT(i) do { } while (0)
+#define PT_FLUSH(sel, off) do { } while (0)
 #endif
 
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
@@ -322,37 +330,36 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
       unsigned* zc = zcnt + 32 * (tz % NB);
       const unsigned target = (unsigned)(TM * (tz / NB + 1));
       if (block) poll_ge(zc, target);
-      else if (ld_relaxed(zc) < target || ld_acquire(zc) < target) return;
+      else if (ld_acquire(zc) < target) return;  // one acquire (a relaxed pre-check cost another L2 round trip)
       if (atomicCAS(&s_w1iss[sl], tz, tz + 1) == tz) issue_w1(tz);
     };
     uint32_t par = 0;
     int tg = 0;
 #pragma unroll 1
     for (int cell = team; cell < ncells; cell += A.nteams) {
+      PT_DECL
 #pragma unroll 1
       for (int t = 0; t < A.T1; t++, tg++) {
         const int T = tg;
-#ifdef FKS_V4_PHASE_TIMING  // tools/phase_timing_v4.py: an instrumented build variant only
-        long long* st = (A.dbg && lane == 0 && (warp == 6 || warp == 0) && cell == team + 2 * A.nteams && t >= 2 && t < 6)
-                            ? A.dbg + (long long)blockIdx.x * 128 + (t - 2) * 16 + (warp == 0 ? 3 : 0) : nullptr;
-#endif
-        STAMP(0);
         if (!isx) {
           // ---------------- Y warp ----------------
           if (lane == 0 && c == 0) try_issue_w1(tg, true);
           mbar_wait(&bar_w1[g], par);
           if (c == 0 && lane == 0) {
-            __threadfence();
-            atomicAdd(ycnt + 32 * (tg % NB), 1u);  // this group has consumed W1(tg)
+            // this group's copy of W1(tg) has landed (observed through the mbarrier), so the buffer may be
+            // refilled: a relaxed count suffices (a fence.sc here cost 2 % of the kernel)
+            atomicAdd(ycnt + 32 * (tg % NB), 1u);
           }
-          STAMP(1);
+          PT(0);  // Y: W1 issue / wait / ack
 #pragma unroll 1
           for (int pl = 0; pl < 2; pl++) {
             double2 u[16];
             xform48((pl ? in1 : in0) + (lane < K ? lane : K - 1) * K, 1, c, u);
             // slot c is free once X(g, c) has parked the rows of term t - 1 (waited after the first transform, so
             // that the park overlaps it)
+            if (pl == 0) PT(1);  // Y: first transform
             if (pl == 0 && T > 0) mbar_wait(&bar_empty[g][c], (T - 1) & 1);
+            if (pl == 0) PT(2);  // Y: slot wait
             if (lane < K) {
               double2* ydst = ybuf(pl, c) + lane;
 #pragma unroll
@@ -360,15 +367,14 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
             }
           }
           __syncwarp();
-          if (lane == 0) {
-            mbar_arrive(&bar_full[g][c]);
-            if (atomicAdd(&s_yall[g], 1) + 1 == 3 * (T + 1)) try_issue_w1(tg + 1, false);  // prefetch
-          }
-          STAMP(2);
+          if (lane == 0) mbar_arrive(&bar_full[g][c]);
+          PT(3);  // Y: stores + second transform + stores
+          if (lane == 0 && atomicAdd(&s_yall[g], 1) + 1 == 3 * (T + 1)) try_issue_w1(tg + 1, false);  // prefetch
+          PT(4);  // Y: signal / prefetch
         } else {
           // ---------------- X warp ----------------
           mbar_wait(&bar_full[g][c], T & 1);
-          STAMP(1);
+          PT(0);  // X: wait for Y
           if (t == 0) {  // first term of the cell: zero the three G blocks
             uint32_t zw[32];
 #pragma unroll
@@ -396,7 +402,7 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
           }
           __syncwarp();
           if (lane == 0) mbar_arrive(&bar_empty[g][c]);  // the Y slot may be refilled
-          STAMP(2);
+          PT(1);  // X: park
 #pragma unroll 1
           for (int rx = 0; rx < 3; rx++) {
             double2 u[16];
@@ -431,7 +437,7 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
             g_accumulate(tX + 32u * rx, u);
           }
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-          STAMP(3);
+          PT(2);  // X: three class tasks
           if (t == A.T1 - 1) {  // G[cell][px = 3q' + rx][pz / 2][py = 3 xq + c][pz % 2]: z-rows interleaved in
                                 // pairs; the virtual plane pz0 + xp holds pz = pfa_p(pz0 + xp)
             const int pz = pfa_p(pz0 + xp);
@@ -448,8 +454,10 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
             }
           }
         }
+        PT(3);  // X: G write-out (last term) / Y: -
         par ^= 1;
       }
+      PT_FLUSH(lane == 0 && (warp == 6 || warp == 0) && cell == team + 2 * A.nteams, warp == 0 ? 8 : 0);
     }
   } else {
     // ---------------------------------------------- Z warps -----------------------------------------------
@@ -470,14 +478,10 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
     for (int cell = team; cell < ncells; cell += A.nteams) {
       mbar_wait(&bar_fh, par_fh);
       par_fh ^= 1;
+      PT_DECL
 #pragma unroll 1
       for (int t = 0; t < A.T1; t++, tg++) {
         const double2* tb = A.tabT + (long long)t * LHN + K * h0;     // the member's table block (L2)
-#ifdef FKS_V4_PHASE_TIMING
-        long long* st = (A.dbg && zt == 0 && cell == team + 2 * A.nteams && t >= 2 && t < 6)
-                            ? A.dbg + (long long)blockIdx.x * 128 + (t - 2) * 16 + 8 : nullptr;
-#endif
-        STAMP(0);
         // Warp 12 publishes W1(tg - 1) (fence + team counter) and waits for the buffer of W1(tg) to be free while
         // warps 13-15 form the products, so neither the store drain nor the poll sits on the Z warps' chain.
         if (zt < 32) {
@@ -525,11 +529,10 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
             }
           }
         }
-        STAMP(1);
+        PT(0);  // Z: products (warps 13-15) / publication + ring poll (warp 12)
         nbar(3, NZT);  // products complete, W1(tg - 1) published, W1(tg)'s buffer free
         if (zt == 0 && t == A.T1 - 1 && cell + A.nteams < ncells) issue_fh(cell + A.nteams);
-        STAMP(2);
-        STAMP(3);
+        PT(1);  // Z: barrier
         double2* W1b = W1t + (tg % NB) * (long long)W1_BUF;
         {  // 4 Z warps: single class tasks tau = r * na + j, 2 rounds of 128 threads cover 3 na <= 246
           const int na = nh + nmir;
@@ -551,8 +554,9 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
           }
         }
         nbar(3, NZT);
-        STAMP(4);
+        PT(2);  // Z: class tasks + stores + barrier
       }
+      PT_FLUSH((zt & 31) == 0 && zt < 64 && cell == team + 2 * A.nteams, zt == 0 ? 24 : 16);
     }
     if (zt == 0 && tg > 0) {  // publish the last term
       __threadfence();

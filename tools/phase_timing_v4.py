@@ -1,5 +1,7 @@
-"""Per-phase cycle counts of the v4 term-loop kernel (FKS_PHASE_TIMING=1; needs the instrumented build variant: FKS_LIB=$(python tools/build_variant.py ptime4 -DFKS_V4_PHASE_TIMING)): YX group 0 and Z warps of every CTA,
-terms 2..5 of the first cell of each team.  Usage: python tools/phase_timing_v4.py [config] [n_cells]"""
+"""Steady-state phase accounting of the N = 32 term-loop kernel: cycles per term spent in each phase by lane 0 of
+Y warp 6, X warp 0 and Z warps 12 / 13 of every CTA, summed over the terms of each team's third cell (needs the
+instrumented build variant: FKS_LIB=$(python tools/build_variant.py ptime4 -DFKS_V4_PHASE_TIMING)).
+Usage: python tools/phase_timing_v4.py [config] [n_cells]   (n_cells >= 3 x 12 teams)"""
 import os
 import sys
 
@@ -12,29 +14,21 @@ from paper_1701_01608_b200 import binding as B  # noqa: E402
 from paper_1701_01608_b200 import inputs  # noqa: E402
 from paper_1701_01608_b200.configs import CONFIGS  # noqa: E402
 
-cfg = CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "c2"]
-n = int(sys.argv[2]) if len(sys.argv) > 2 else cfg.n_cells
+cfg = CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "c3"]
+n = int(sys.argv[2]) if len(sys.argv) > 2 else 1440
 f = inputs.make_f(cfg, device="cuda", cells=list(range(n)))
 col = B.Collision(cfg.N, cfg.L, cfg.M, cfg.M_r, cfg.kernel)
-print("layout", col.info)
 Q = col.collision_batch(f)
 torch.cuda.synchronize()
-buf = B.fks_debug_timestamps(col.h)
-raw = buf[: 144 * 128].reshape(144, 8, 16)[:, :4, :]  # [cta][term][slot]
-raw = raw[raw[:, 0, 0] > 0]
-yx, z = raw[:, :, :8].astype(float), raw[:, :, 8:].astype(float)
-print("CTAs sampled:", len(raw))
-for name, a, b in [("Y: wait W1 (poll + TMA)", 0, 1), ("Y: slot wait + 2 tasks", 1, 2),
-                   ("X: wait Y", 3, 4), ("X: park", 4, 5), ("X: 3 tasks", 5, 6)]:
-    d = yx[:, :, b] - yx[:, :, a]
-    print(f"{name:28s} median {np.median(d):8.0f}  p10 {np.percentile(d, 10):8.0f}  p90 {np.percentile(d, 90):8.0f}")
-d = yx[:, 1:, 3] - yx[:, :-1, 3]
-print(f"{'X term period':28s} median {np.median(d):8.0f}")
-d = yx[:, 1:, 0] - yx[:, :-1, 0]
-print(f"{'YX term period':28s} median {np.median(d):8.0f}")
-for name, a, b in [("Z: products (zt 0)", 0, 1), ("Z: barrier + publish", 1, 2), ("Z: wait W1 buffer free", 2, 3),
-                   ("Z: class tasks + stores", 3, 4)]:
-    d = z[:, :, b] - z[:, :, a]
-    print(f"{name:28s} median {np.median(d):8.0f}  p10 {np.percentile(d, 10):8.0f}  p90 {np.percentile(d, 90):8.0f}")
-d = z[:, 1:, 0] - z[:, :-1, 0]
-print(f"{'Z term period':28s} median {np.median(d):8.0f}")
+T1 = col.info["T"] + 1
+buf = B.fks_debug_timestamps(col.h)[: 144 * 128].reshape(144, 128).astype(float) / T1
+roles = [("Y warp 6", 0, ["W1 issue/wait/ack", "first transform", "slot wait", "stores + 2nd transform",
+                          "signal/prefetch"]),
+         ("X warp 0", 8, ["wait for Y", "park", "3 class tasks", "G write-out"]),
+         ("Z warp 13", 16, ["products", "barrier", "class tasks + barrier"]),
+         ("Z warp 12", 24, ["publish + ring poll", "barrier", "class tasks + barrier"])]
+print(f"cycles per term (median over {len(buf)} CTAs; terms of each team's third cell), T+1 = {T1}")
+for name, off, labels in roles:
+    tot = buf[:, off:off + len(labels)].sum(1)
+    parts = "  ".join(f"{lab} {np.median(buf[:, off + i]):6.0f}" for i, lab in enumerate(labels))
+    print(f"{name:10s} period {np.median(tot):6.0f} | {parts}")
