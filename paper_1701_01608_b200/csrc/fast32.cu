@@ -457,7 +457,8 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
         PT(3);  // X: G write-out (last term) / Y: -
         par ^= 1;
       }
-      PT_FLUSH(lane == 0 && (warp == 6 || warp == 0) && cell == team + 2 * A.nteams, warp == 0 ? 8 : 0);
+      PT_FLUSH(lane == 0 && (warp == 6 || warp == 7 || warp == 0) && cell == team + 2 * A.nteams,
+               warp == 0 ? 8 : (warp == 6 ? 0 : 32));
     }
   } else {
     // ---------------------------------------------- Z warps -----------------------------------------------

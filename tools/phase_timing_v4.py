@@ -1,5 +1,5 @@
 """Steady-state phase accounting of the N = 32 term-loop kernel: cycles per term spent in each phase by lane 0 of
-Y warp 6, X warp 0 and Z warps 12 / 13 of every CTA, summed over the terms of each team's third cell (needs the
+Y warps 6 (class 0) and 7 (class 1), X warp 0 and Z warps 12 / 13 of every CTA, summed over the terms of each team's third cell (needs the
 instrumented build variant: FKS_LIB=$(python tools/build_variant.py ptime4 -DFKS_V4_PHASE_TIMING)).
 Usage: python tools/phase_timing_v4.py [config] [n_cells]   (n_cells >= 3 x 12 teams)"""
 import os
@@ -24,6 +24,8 @@ T1 = col.info["T"] + 1
 buf = B.fks_debug_timestamps(col.h)[: 144 * 128].reshape(144, 128).astype(float) / T1
 roles = [("Y warp 6", 0, ["W1 issue/wait/ack", "first transform", "slot wait", "stores + 2nd transform",
                           "signal/prefetch"]),
+         ("Y warp 7", 32, ["W1 issue/wait/ack", "first transform", "slot wait", "stores + 2nd transform",
+                           "signal/prefetch"]),
          ("X warp 0", 8, ["wait for Y", "park", "3 class tasks", "G write-out"]),
          ("Z warp 13", 16, ["products", "barrier", "class tasks + barrier"]),
          ("Z warp 12", 24, ["publish + ring poll", "barrier", "class tasks + barrier"])]
