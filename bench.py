@@ -552,9 +552,10 @@ def main():
                      "flop_per_cell": fl["hot"], "cells_per_launch": cells_per_launch, "ms_per_launch": hot_ms,
                      "frac_of_measured_dfma": achieved / 36.66,
                      "peak_at_max_clock": fp64_peak_tflops(1965.0),
-                     # the N = 32 kernel has shown two stable operating points from build to build (about 444 and
-                     # 472 ns per cell and term: 160 / 170 ms per 10 923-cell c3 launch): record which
-                     "operating_point": (("fast" if hot_ms * 1e6 / (cells_per_launch * (T + 1)) < 457.0 else "slow")
+                     # the N = 32 kernel is sensitive to how its warp roles phase-lock; the shipped
+                     # build runs at about 375 ns per cell and term (137 ms per 10 923-cell c3 launch): record
+                     # whether this run landed there or on a slower point
+                     "operating_point": (("fast" if hot_ms * 1e6 / (cells_per_launch * (T + 1)) < 395.0 else "slow")
                                          if cfg.N == 32 and col.info.get("path") == 2 else None),
                      "ns_per_cell_term": hot_ms * 1e6 / (cells_per_launch * (T + 1)),
                      "peak_note": f"FP64 DFMA unit counts: 148 SM x 64 lanes x 2 flop x {sm_used:.0f} MHz (median SM "
