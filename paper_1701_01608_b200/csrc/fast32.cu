@@ -112,7 +112,11 @@ struct Args {
 #define PT(i) do { const long long pt_n = clock64(); pt_acc[i] += pt_n - pt_last; pt_last = pt_n; } while (0)
 #define PT_FLUSH(sel, off) do { if ((sel) && A.dbg) for (int pt_i = 0; pt_i < 6; pt_i++) \
     A.dbg[(long long)blockIdx.x * 128 + (off) + pt_i] = pt_acc[pt_i]; } while (0)
+// pins a transform's results before a stamp, so that the stamp does not fall inside the transform
+#define PT_HOLD(u) do { for (int pt_i = 0; pt_i < 16; pt_i += 2) \
+    asm volatile("" : "+d"(u[pt_i].x), "+d"(u[pt_i].y), "+d"(u[pt_i + 1].x), "+d"(u[pt_i + 1].y) :: "memory"); } while (0)
 #else
+#define PT_HOLD(u) do { } while (0)
 #define PT_DECL
 #define PT(i) do { } while (0)
 #define PT_FLUSH(sel, off) do { } while (0)
@@ -355,20 +359,21 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
           for (int pl = 0; pl < 2; pl++) {
             double2 u[16];
             xform48((pl ? in1 : in0) + (lane < K ? lane : K - 1) * K, 1, c, u);
+            PT_HOLD(u);
+            PT(1);  // Y: transforms
             // slot c is free once X(g, c) has parked the rows of term t - 1 (waited after the first transform, so
             // that the park overlaps it)
-            if (pl == 0) PT(1);  // Y: first transform
             if (pl == 0 && T > 0) mbar_wait(&bar_empty[g][c], (T - 1) & 1);
-            if (pl == 0) PT(2);  // Y: slot wait
+            PT(2);  // Y: slot wait
             if (lane < K) {
               double2* ydst = ybuf(pl, c) + lane;
 #pragma unroll
               for (int q = 0; q < 16; q++) ydst[q * K] = u[fftd::qslot(q)];
             }
+            PT(3);  // Y: stores
           }
           __syncwarp();
           if (lane == 0) mbar_arrive(&bar_full[g][c]);
-          PT(3);  // Y: stores + second transform + stores
           if (lane == 0 && atomicAdd(&s_yall[g], 1) + 1 == 3 * (T + 1)) try_issue_w1(tg + 1, false);  // prefetch
           PT(4);  // Y: signal / prefetch
         } else {

@@ -22,10 +22,8 @@ Q = col.collision_batch(f)
 torch.cuda.synchronize()
 T1 = col.info["T"] + 1
 buf = B.fks_debug_timestamps(col.h)[: 144 * 128].reshape(144, 128).astype(float) / T1
-roles = [("Y warp 6", 0, ["W1 issue/wait/ack", "first transform", "slot wait", "stores + 2nd transform",
-                          "signal/prefetch"]),
-         ("Y warp 7", 32, ["W1 issue/wait/ack", "first transform", "slot wait", "stores + 2nd transform",
-                           "signal/prefetch"]),
+roles = [("Y warp 6", 0, ["W1 issue/wait/ack", "2 transforms", "slot wait", "2 x 16 stores", "signal/prefetch"]),
+         ("Y warp 7", 32, ["W1 issue/wait/ack", "2 transforms", "slot wait", "2 x 16 stores", "signal/prefetch"]),
          ("X warp 0", 8, ["wait for Y", "park", "3 class tasks", "G write-out"]),
          ("Z warp 13", 16, ["products", "barrier", "class tasks + barrier"]),
          ("Z warp 12", 24, ["publish + ring poll", "barrier", "class tasks + barrier"])]
