@@ -29,7 +29,8 @@ using fftd::dif_combine;
 using fftd::fft16;
 using fftd::qslot;
 
-constexpr int PL8 = 8;  // planes (or pencil groups) per CTA in kf1 / kf2 / kb3
+constexpr int PL8 = 8;  // planes (or pencil groups) per CTA in kf1 / kf2 / kb3 (3 CTAs per SM: the launch bounds
+                        // cap them at 85 registers; kf1 -16 %, kf2 -11 %, kb3 -2.5 % against the register-limited 2)
 constexpr int PB1 = 4;  // px planes per CTA in kb1
 constexpr int PB2 = 4;  // ky columns per CTA in kb2
 constexpr int RS = 17;  // padded row stride (double2) of 16-element rows
@@ -79,7 +80,7 @@ __device__ __forceinline__ void gather_tables(const GatherSrc& g, long long j, i
   }
 }
 
-__global__ void __launch_bounds__(256) kf1(const double* __restrict__ f, double2* __restrict__ F2, const GatherSrc g,
+__global__ void __launch_bounds__(256, 3) kf1(const double* __restrict__ f, double2* __restrict__ F2, const GatherSrc g,
                                            int gather) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* buf = reinterpret_cast<double2*>(smem_raw);  // [8][32][RS] (rows padded: conflict-free row tasks)
@@ -154,7 +155,7 @@ __device__ __forceinline__ int lh_offset(int pp, int iz, int nb) {
 
 // kf2: CTA = 8 consecutive (cell, ly) columns.  x: FFT32 over jx -> lx in K', times N^-3; writes f^ at +l and
 // (for lz > 0) its conjugate at -l, lower-half pencils only.
-__global__ void __launch_bounds__(256) kf2(const double2* __restrict__ F2, double2* __restrict__ fhT, long long ncol, int nb) {
+__global__ void __launch_bounds__(256, 3) kf2(const double2* __restrict__ F2, double2* __restrict__ fhT, long long ncol, int nb) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* buf = reinterpret_cast<double2*>(smem_raw);  // [8][32 jx][16 lz]
   const int tid = threadIdx.x;
@@ -312,7 +313,7 @@ __global__ void __launch_bounds__(192) kb2(const double2* __restrict__ H2, doubl
 
 // kb3: CTA = (cell, 8 jx planes).  z: inverse FFT32 over kz -> jz;  y: Hermitian -> real inverse FFT32 (packed
 // FFT16); then Q or f* + s Q, transposed through shared memory into coalesced stores.
-__global__ void __launch_bounds__(256) kb3(const double2* __restrict__ E1, const double* fin, double* out,
+__global__ void __launch_bounds__(256, 3) kb3(const double2* __restrict__ E1, const double* fin, double* out,
                                            int euler, double s, const GatherSrc g, int gather, double* mpart,
                                            double L, double hv) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
