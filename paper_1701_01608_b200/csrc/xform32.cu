@@ -31,7 +31,8 @@ using fftd::qslot;
 
 constexpr int PL8 = 8;  // planes (or pencil groups) per CTA in kf1 / kf2 / kb3 (3 CTAs per SM: the launch bounds
                         // cap them at 85 registers; kf1 -16 %, kf2 -11 %, kb3 -2.5 % against the register-limited 2)
-constexpr int PB1 = 4;  // px planes per CTA in kb1
+constexpr int PB1 = 4;  // px planes per CTA in kb1 (2 measured the same, 1 30 % slower)
+constexpr int KB1_T = 72 * PB1;  // kb1 threads: (class, plane, row pair)
 constexpr int PB2 = 4;  // ky columns per CTA in kb2
 constexpr int RS = 17;  // padded row stride (double2) of 16-element rows
 constexpr int ZS = 49;  // padded row stride (double2) of 48-element rows
@@ -198,7 +199,7 @@ __global__ void __launch_bounds__(256, 3) kf2(const double2* __restrict__ F2, do
 // kb1: CTA = (cell, 4 px planes), 288 threads.  First axis (py, contiguous): two real rows packed as one
 // complex row, FFT48, untangled on the fly (ky = 0..15);  second axis (pz): FFT48 -> kz in K'.
 // Out H2[cell][px][kz][ky].
-__global__ void __launch_bounds__(288, 2) kb1(const double* __restrict__ G, double2* __restrict__ H2) {
+__global__ void __launch_bounds__(KB1_T, 8 / PB1) kb1(const double* __restrict__ G, double2* __restrict__ H2) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   // [4 planes][24 row pairs][ZS]: element py of the pair = (G(pz = 2pr, py), G(pz = 2pr+1, py)); then in
   // place the complex FFT48 of the pair
@@ -209,7 +210,7 @@ __global__ void __launch_bounds__(288, 2) kb1(const double* __restrict__ G, doub
   {  // G holds each pair of z-rows interleaved: (G(2pr, py), G(2pr+1, py)) is one 16-byte element
     const double2* src = reinterpret_cast<const double2*>(G + (cell * P + px0) * P * P);
 #pragma unroll 4
-    for (int i = tid; i < PB1 * P * P / 2; i += 288) {
+    for (int i = tid; i < PB1 * P * P / 2; i += KB1_T) {
       const int pr = i / P, col = i - pr * P;  // pr = s * 24 + row pair, col = py
       cp16(zc + pr * ZS + col, src + i);
     }
@@ -217,7 +218,7 @@ __global__ void __launch_bounds__(288, 2) kb1(const double* __restrict__ G, doub
   cp_wait_all();
   __syncthreads();
   {  // z: thread = (class r, plane, row pair)
-    const int r = tid / 96, s = (tid % 96) / 24, pr = tid % 24;
+    const int r = tid / (24 * PB1), s = (tid % (24 * PB1)) / 24, pr = tid % 24;
     double2* zrow = zc + (s * 24 + pr) * ZS;
     InCol in{zrow, 1};
     double2 u[16];
@@ -230,8 +231,8 @@ __global__ void __launch_bounds__(288, 2) kb1(const double* __restrict__ G, doub
     for (int q = 0; q < 16; q++) zrow[3 * q + r] = u[qslot(q)];
   }
   __syncthreads();
-  if (tid < 192) {  // y: thread = (class r, plane, kz)
-    const int r = tid >> 6, s = (tid >> 4) & 3, kz = tid & 15;
+  if (tid < 48 * PB1) {  // y: thread = (class r, plane, kz)
+    const int r = tid / (16 * PB1), s = (tid / 16) % PB1, kz = tid & 15;
     struct InUntangle {  // H1(py, kz): even py -> first row of the pair, odd py -> second row
       const double2* z; int kz;
       __device__ __forceinline__ bool nz(int) const { return true; }
@@ -493,7 +494,7 @@ void xform32_back(Ctx& c, const double* G, double2* scratch_a, double2* scratch_
   const long long ncol = n * K;
   GatherSrc g{};
   if (gs) g = *gs;
-  kb1<<<(unsigned)(n * (P / PB1)), 288, PB1 * 24 * ZS * 16, st>>>(G, scratch_a);
+  kb1<<<(unsigned)(n * (P / PB1)), KB1_T, PB1 * 24 * ZS * 16, st>>>(G, scratch_a);
   kb2<<<(unsigned)((ncol + PB2 - 1) / PB2), 192, PB2 * (P + K) * H * 16, st>>>(scratch_a, scratch_b, ncol, c.p.project_mass);
   kb3<<<(unsigned)(n * (N / PL8)), 256, PL8 * N * RS * 16, st>>>(scratch_b, fin, out, euler ? 1 : 0, s, g, gs ? 1 : 0,
                                                                   mpart, c.p.L, 2.0 * c.p.L / N);
