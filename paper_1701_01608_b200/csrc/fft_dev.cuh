@@ -134,17 +134,17 @@ __device__ __forceinline__ void fft16i(double2 (&u)[16]) {
 // transform then leaves z(k) at slot k2 with k = 3 pfa_q(r, k2) + r.
 __host__ __device__ __forceinline__ constexpr int pfa_q(int r, int k2) { return (5 * r + 11 * k2) & 15; }
 __host__ __device__ __forceinline__ constexpr int pfa_n2(int m) { return (11 * m) & 15; }  // m = 3 n2 mod 16
-// u[pfa_n2(m)] from a = Z(m), v = Z(m - 16), m = 1..15; r != 0 with sg = +sin(2pi/3) (r = 1) or - (r = 2)
-// (m is a constant after unrolling, so the branch folds)
-__device__ __forceinline__ double2 pfa_combine(int m, double2 a, double2 v, double sg) {
+// u[pfa_n2(m)] from a = Z(m), v = Z(m - 16), m = 1..15 (m is a constant after unrolling, so the branch folds), with
+// w = w3^{2r} = (cr, -sg): r = 1, 2: cr = -1/2, sg = +-sin(2pi/3); r = 0: cr = 1, sg = 0 (every case reduces to a + v)
+__device__ __forceinline__ double2 pfa_combine(int m, double2 a, double2 v, double cr, double sg) {
   const int j = (3 * pfa_n2(m)) >> 4;
-  if (j == 0) {  // a + w v, w = w3^{2r} = (-1/2, -sg)
-    return make_double2(fma(sg, v.y, fma(-0.5, v.x, a.x)), fma(-sg, v.x, fma(-0.5, v.y, a.y)));
+  if (j == 0) {  // a + w v
+    return make_double2(fma(sg, v.y, fma(cr, v.x, a.x)), fma(-sg, v.x, fma(cr, v.y, a.y)));
   } else if (j == 2) {  // conj(w) a + v
-    return make_double2(fma(-sg, a.y, fma(-0.5, a.x, v.x)), fma(sg, a.x, fma(-0.5, a.y, v.y)));
+    return make_double2(fma(-sg, a.y, fma(cr, a.x, v.x)), fma(sg, a.x, fma(cr, a.y, v.y)));
   } else {  // w a + conj(w) v
     const double sx = a.x + v.x, sy = a.y + v.y, dx = a.x - v.x, dy = a.y - v.y;
-    return make_double2(fma(-0.5, sx, sg * dy), fma(-0.5, sy, -sg * dx));
+    return make_double2(fma(cr, sx, sg * dy), fma(cr, sy, -sg * dx));
   }
 }
 

@@ -35,7 +35,7 @@ __device__ __forceinline__ void x_gt(const double2* base, int ld, int r, double2
   } else {
     const double sg = (r == 1) ? 0.86602540378443864676 : -0.86602540378443864676;
 #pragma unroll
-    for (int m = 1; m < 16; m++) u[fftd::pfa_n2(m)] = fftd::pfa_combine(m, base[(m + 15) * ld], base[(m - 1) * ld], sg);
+    for (int m = 1; m < 16; m++) u[fftd::pfa_n2(m)] = fftd::pfa_combine(m, base[(m + 15) * ld], base[(m - 1) * ld], -0.5, sg);
   }
   fftd::fft16i(u);
 }
