@@ -553,8 +553,11 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
             xform48_gt((mir ? zm : zp) + jj, nh, r, u);
             if (act) {
               const int pp = mir ? (NPEN - 1) - (h0 + jj) : h0 + jj;
+              // one 64-bit base per task, the plane offsets q NPEN as immediates (an int index per store cost five
+              // address instructions each)
+              double2* dst = W1b + (16 * r * NPEN + pp);
 #pragma unroll
-              for (int q = 0; q < 16; q++) W1b[(16 * r + q) * NPEN + pp] = u[fftd::qslot(q)];  // virtual plane
+              for (int q = 0; q < 16; q++) dst[q * NPEN] = u[fftd::qslot(q)];  // virtual plane 16 r + q
             }
           }
         }
