@@ -185,36 +185,16 @@ struct InK {
 
 // Pruned inverse transform of one output class r (runtime, warp-uniform): z(3q + r) = sum_{l=-15..15} Z(l)
 // e^{2 pi i l (3q + r)/48}, inputs Z(l) at base[(l + 15) * ld].  Two forms (fft_dev.cuh):
-//   xform48     radix-3 DIF combine (only l mod 48 in 0..15 and 33..47 are present) with the twiddles w48^{rm},
-//               then FFT16; z(3q + r) ends in u[qslot(q)].  Used by the Y warps (and, inlined, the X warps).
-//   xform48_gt  Good-Thomas form: no inter-stage twiddles, the 16-point stage in tangent form (-16 % FP64
-//               instructions); slot k2 ends in u[qslot(k2)] and holds z(3 pfa_q(r, k2) + r).  Used by the Z warps,
-//               whose outputs go to "virtual" W1 planes v = 16 r + k2 (pz = pfa_p(v), mapped back at the G
-//               write-out).  In the Y and X roles the same form measured slower (profiles/r02_experiments.txt).
-// ONE instance per warp role keeps the kernel's hot code inside the instruction cache (templated per-class copies
-// thrashed it: ncu no_instruction stalls).
-__device__ __forceinline__ void xform48(const double2* base, int ld, int r, double2 (&u)[16]) {
-  u[0] = base[15 * ld];
-  if (r == 0) {
-#pragma unroll
-    for (int m = 1; m < 16; m++) u[m] = fftd::cadd(base[(m + 15) * ld], base[(m - 1) * ld]);
-  } else {
-    // w3^{2r} = (-1/2, -+ sin(2pi/3)) for r = 1, 2;  twiddle w48^{r m}
-    const double sg = (r == 1) ? -0.86602540378443864676 : 0.86602540378443864676;
-    const double2* tw = fftd::c_tw48;
-#pragma unroll
-    for (int m = 1; m < 16; m++) {
-      const double2 a = base[(m + 15) * ld], v = base[(m - 1) * ld];
-      double2 acc;
-      acc.x = fma(-0.5, v.x, a.x);
-      acc.x = fma(-sg, v.y, acc.x);
-      acc.y = fma(-0.5, v.y, a.y);
-      acc.y = fma(sg, v.x, acc.y);
-      u[m] = fftd::cmul_s<1>(tw[r * m], acc);
-    }
-  }
-  fftd::fft16<1>(u);
-}
+//   xform48_gt  Good-Thomas form (Y and Z warps): no inter-stage twiddles, the 16-point stage in tangent form, one
+//               code path for the three classes; slot k2 ends in u[qslot(k2)] and holds z(3 pfa_q(r, k2) + r).  The
+//               Z warps store slot k2 of class r to the "virtual" W1 plane v = 16 r + k2 and the Y warps to row k2
+//               of their class slot; the Y and X passes do not care which pz / py a plane or row holds, so only the
+//               G write-out maps them back (pz = pfa_p(v), py = pfa_p(16 c + xq)).
+//   DIF         radix-3 decimation-in-frequency combine with the twiddles w48^{rm}, then FFT16; z(3q + r) ends in
+//               u[qslot(q)].  The X warps (inlined, inputs from TMEM): there the Good-Thomas form measured slower.
+// The choice per role is set by the instruction cache as much as by the FP64 count: the hot loops of the three roles
+// share it and sit at its edge (profiles/r02_experiments.txt r2ae-r2ap).  ONE instance per warp role
+// keeps the kernel's hot code small (templated per-class copies thrashed the cache: ncu no_instruction stalls).
 __device__ __forceinline__ void xform48_gt(const double2* base, int ld, int r, double2 (&u)[16]) {
   // one code path for every class: class 0 is the same combine with the rotation w = 1 (the Z code is 1.1 KB smaller
   // than with a separate class-0 loop, which measured 0.4 % faster despite the extra FP64 of the class-0 tasks: the
@@ -357,7 +337,7 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
 #pragma unroll 1
           for (int pl = 0; pl < 2; pl++) {
             double2 u[16];
-            xform48((pl ? in1 : in0) + (lane < K ? lane : K - 1) * K, 1, c, u);
+            xform48_gt((pl ? in1 : in0) + (lane < K ? lane : K - 1) * K, 1, c, u);
             PT_HOLD(u);
             PT(1);  // Y: transforms
             // slot c is free once X(g, c) has parked the rows of term t - 1 (waited after the first transform, so
@@ -410,6 +390,12 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
 #pragma unroll 1
           for (int rx = 0; rx < 3; rx++) {
             double2 u[16];
+                u[fftd::pfa_n2(m)] = fftd::pfa_combine(m, vb, va, cr, sg);
+#endif
+              }
+            }
+            fftd::fft16i(u);
+#else
             const double sg = (rx == 1) ? -0.86602540378443864676 : 0.86602540378443864676;
 #pragma unroll
             for (int mm = 0; mm < 4; mm++) {
@@ -445,7 +431,7 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
           if (t == A.T1 - 1) {  // G[cell][px = 3q' + rx][pz / 2][py = 3 xq + c][pz % 2]: z-rows interleaved in
                                 // pairs; the virtual plane pz0 + xp holds pz = pfa_p(pz0 + xp)
             const int pz = pfa_p(pz0 + xp);
-            const int py = 3 * xq + c;
+            const int py = pfa_p(16 * c + xq);
             double* Gc = A.G + cell * (long long)(P * P * P) + (long long)(pz >> 1) * (2 * P) + (pz & 1) + 2 * py;
 #pragma unroll 1
             for (int rx = 0; rx < 3; rx++) {
