@@ -390,12 +390,6 @@ __global__ void __launch_bounds__(NTHR, 1) hot_kernel_v4(Args A) {
 #pragma unroll 1
           for (int rx = 0; rx < 3; rx++) {
             double2 u[16];
-                u[fftd::pfa_n2(m)] = fftd::pfa_combine(m, vb, va, cr, sg);
-#endif
-              }
-            }
-            fftd::fft16i(u);
-#else
             const double sg = (rx == 1) ? -0.86602540378443864676 : 0.86602540378443864676;
 #pragma unroll
             for (int mm = 0; mm < 4; mm++) {
