@@ -567,6 +567,11 @@ def main():
                        "hbm_bytes_per_cell": 16 * cfg.N ** 3},
         "phases_ms_per_step": {"transport": ph_ms[0] / args.steps, "forward": ph_ms[1] / args.steps,
                                "term_loop": ph_ms[2] / args.steps, "back": ph_ms[3] / args.steps},
+        "phases_note": ("chunk pipeline: the forward / back transforms of neighbouring workspace chunks run on a "
+                        "low-priority stream beside the term-loop launches (on the 4 SMs the 12-CTA teams leave "
+                        "free and in each launch's tail), so their intervals overlap the term loop and do not add "
+                        "up to ms_per_step") if (cfg.N == 32 and ph_cnt[2] > args.steps
+                                                 and not os.environ.get("FKS_NO_PIPELINE")) else None,
         "path": {1: "generic", 2: "fast"}.get(col.info.get("path"), None),
         "fast_layout": {"ctas_per_cell": col.info.get("ctas_per_cell"), "concurrent_cells": col.info.get("concurrent_cells")},
         "clocks": clocks, "gpu_launches": launches, "e2e": e2e, "decomposed": decomposed,

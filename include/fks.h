@@ -75,7 +75,10 @@ typedef struct {
   double cutoff_ratio;          /* Carleman cutoff R_c = ratio*R: 0 (default) or in [1, 1.7071] (A7);
                                    1 = paper-literal; ratios in (0, 1) are rejected (FKS_ERR_INVALID)        */
   int project_mass;             /* 1 = set Q^_0 := 0 exactly (A24); default 0                              */
-  long long max_cells_in_flight;/* workspace limit in cells per chunk; 0 = auto                            */
+  long long max_cells_in_flight;/* workspace limit in cells per chunk; 0 = auto.  On the N = 32 path a batch
+                                   of more than one chunk uses two chunk slots (2x the workspace) so that the
+                                   transforms of neighbouring chunks overlap the term loop (FKS_NO_PIPELINE=1
+                                   in the environment at init turns this off)                              */
   int path;                     /* fks_path                                                                */
   double vhs_alpha;             /* FKS_KERNEL_VHS: exponent a in [0, 1]                                    */
   double vhs_C;                 /* FKS_KERNEL_VHS: C_a > 0; 0 = 1/(4 pi) (a = 0 is then Maxwell molecules) */

@@ -586,6 +586,7 @@ fks_status fast_prepare(Ctx& c) {
   if (per_sm < 1) { set_error("hot kernel does not fit on one SM"); return FKS_ERR_UNSUPPORTED; }
   c.fast_kernel = 4;
   c.fast_variant = v4::TM;
+  c.pipeline = std::getenv("FKS_NO_PIPELINE") == nullptr;
   c.fast_nteams = c.num_sms / v4::TM;
   if (c.fast_nteams < 1) { set_error("fewer SMs than one team"); return FKS_ERR_UNSUPPORTED; }
   e = cudaMalloc(&c.d_ctr, (size_t)c.fast_nteams * v4::CTR_STRIDE * sizeof(unsigned));
@@ -600,6 +601,56 @@ fks_status fast_prepare(Ctx& c) {
   return cuda_status(cudaDeviceSynchronize(), "fast prepare");
 }
 
+namespace {
+// One workspace chunk of `cap` cells: f^T [cap][K^3] complex | scratch [cap][P*K*16] complex | G [cap][P^3] fp64
+// (the back transform reuses f^T as its second scratch buffer).
+struct Slot {
+  double2* fhT; double2* scratch; double* G;
+};
+Slot slot_at(void* base, long long cap) {
+  using namespace f32;
+  Slot sl;
+  sl.fhT = reinterpret_cast<double2*>(base);
+  sl.scratch = sl.fhT + cap * K * NPEN;
+  sl.G = reinterpret_cast<double*>(sl.scratch + cap * (long long)P * K * 16);
+  return sl;
+}
+
+fks_status hot_launch(Ctx& c, const Slot& sl, long long n, cudaStream_t st) {
+  using namespace f32;
+  const long long nt = std::min<long long>(c.fast_nteams, n);
+  v4::Args A{sl.fhT, c.d_abT, sl.G, c.d_w1, c.d_ctr, n, c.T + 1, (int)nt, c.dbg};
+  cudaMemsetAsync(c.d_ctr, 0, (size_t)c.fast_nteams * v4::CTR_STRIDE * sizeof(unsigned), st);
+  void* args[] = {&A};
+  // cooperative launch: the teams spin on each other's counters, so every CTA must be co-resident
+  cudaError_t e = cudaLaunchCooperativeKernel((void*)v4::hot_kernel_v4, dim3((unsigned)(nt * v4::TM)),
+                                              dim3(v4::NTHR), args, v4::SMEM_B, st);
+  if (e != cudaSuccess) return cuda_status(e, "cooperative hot kernel launch");
+  c.launches++;
+  return cuda_status(cudaPeekAtLastError(), "fast hot kernel launch");
+}
+
+// moment partials of `n` cells (kb3's epilogue, N / 8 per cell)
+fks_status ensure_mpart(Ctx& c, long long n) {
+  const size_t need = (size_t)n * (f32::N / 8) * 5;
+  if (need <= c.mpart_elems) return FKS_OK;
+  if (c.d_mpart) cudaFree(c.d_mpart);
+  c.d_mpart = nullptr;
+  c.mpart_elems = 0;
+  cudaError_t e = cudaMalloc(&c.d_mpart, need * sizeof(double));
+  if (e != cudaSuccess) { cudaGetLastError(); return cuda_status(e, "moment partials"); }
+  c.mpart_elems = need;
+  return FKS_OK;
+}
+
+void back_chunk(Ctx& c, const Slot& sl, const double* fin, double* out, long long n, bool euler, double s,
+                cudaStream_t st, const GatherSrc* gs, double* U, double* W) {
+  double* mpart = (U || W) ? c.d_mpart : nullptr;  // moments of the step's output, reduced in kb3's epilogue
+  xform32_back(c, sl.G, sl.scratch, sl.fhT, fin, out, n, euler, s, st, gs, mpart);
+  if (mpart) launch_moments_finish(c, mpart, f32::N / 8, n, U, W, st);
+}
+}  // namespace
+
 fks_status fast_collision(Ctx& c, const double* fin, double* out, long long n, bool euler, double s,
                           cudaStream_t st, const GatherSrc* gs, double* U, double* W) {
   if (c.N != 32) {
@@ -607,49 +658,95 @@ fks_status fast_collision(Ctx& c, const double* fin, double* out, long long n, b
     if (!rc && (U || W)) rc = launch_macro(c, 0, out, nullptr, U, W, n, 0.0, nullptr, st);  // separate moments pass
     return rc;
   }
-  using namespace f32;
-  // workspace: f^T [n][K^3] complex | scratch [n][P*K*16] complex | G [n][P^3] fp64
-  double2* fhT = reinterpret_cast<double2*>(c.d_ws);
-  double2* scratch = fhT + n * K * NPEN;
-  double* G = reinterpret_cast<double*>(scratch + n * (long long)P * K * 16);
+  const Slot sl = slot_at(c.d_ws, n);
+  if (U || W) {
+    fks_status rc = ensure_mpart(c, n);
+    if (rc) return rc;
+  }
   c.prof.begin(1, st);
-  xform32_forward(c, fin, fhT, scratch, n, c.fast_variant, st, gs);
+  xform32_forward(c, fin, sl.fhT, sl.scratch, n, c.fast_variant, st, gs);
   c.prof.end(1, st);
-
   c.prof.begin(2, st);
-  {
-    const long long nt = std::min<long long>(c.fast_nteams, n);
-    v4::Args A{fhT, c.d_abT, G, c.d_w1, c.d_ctr, n, c.T + 1, (int)nt, c.dbg};
-    cudaMemsetAsync(c.d_ctr, 0, (size_t)c.fast_nteams * v4::CTR_STRIDE * sizeof(unsigned), st);
-    void* args[] = {&A};
-    // cooperative launch: the teams spin on each other's counters, so every CTA must be co-resident
-    cudaError_t e = cudaLaunchCooperativeKernel((void*)v4::hot_kernel_v4, dim3((unsigned)(nt * v4::TM)),
-                                                dim3(v4::NTHR), args, v4::SMEM_B, st);
-    if (e != cudaSuccess) { c.prof.end(2, st); return cuda_status(e, "cooperative hot kernel launch"); }
-  }
-  c.launches++;
+  fks_status rc = hot_launch(c, sl, n, st);
   c.prof.end(2, st);
-  fks_status rc = cuda_status(cudaPeekAtLastError(), "fast hot kernel launch");
   if (rc) return rc;
-
   c.prof.begin(3, st);
-  double* mpart = nullptr;
-  if (U || W) {  // moments of the step's output, reduced in kb3's epilogue (N / 8 partials per cell)
-    const size_t need = (size_t)n * (N / 8) * 5;
-    if (need > c.mpart_elems) {
-      if (c.d_mpart) cudaFree(c.d_mpart);
-      c.d_mpart = nullptr;
-      c.mpart_elems = 0;
-      cudaError_t e = cudaMalloc(&c.d_mpart, need * sizeof(double));
-      if (e != cudaSuccess) { cudaGetLastError(); c.prof.end(3, st); return cuda_status(e, "moment partials"); }
-      c.mpart_elems = need;
-    }
-    mpart = c.d_mpart;
-  }
-  xform32_back(c, G, scratch, fhT, fin, out, n, euler, s, st, gs, mpart);
-  if (mpart) launch_moments_finish(c, mpart, N / 8, n, U, W, st);
+  back_chunk(c, sl, fin, out, n, euler, s, st, gs, U, W);
   c.prof.end(3, st);
   return cuda_status(cudaPeekAtLastError(), "fast collision");
+}
+
+bool fast_pipeline_ok(const Ctx& c) { return c.N == 32 && c.P == 48 && c.pipeline; }
+
+// Chunks k = 0..nc-1 alternate between two workspace slots.  Stream order (host issue order fwd0, fwd1, then per k:
+// hot(k), back(k), fwd(k+2)):
+//   hot stream  (highest priority): [wait fwd(k)] hot(k) [record hot(k)]
+//   side stream (lowest priority):  fwd(0) fwd(1) back(0) fwd(2) back(1) fwd(3) ... back(nc-1)
+// back(k) waits for hot(k); fwd(k+2) reuses slot k % 2 after back(k) on the same stream, and hot(k+2) waits for
+// fwd(k+2), so every hazard on a slot is ordered.  The 12-CTA teams of the term-loop kernel occupy 144 of the 148
+// SMs; the transforms of the neighbouring chunks run on the other 4 (and on the SMs each team frees at the end of a
+// launch), while the priority puts the next term-loop launch's CTAs first whenever SMs free up.  A chunk may name
+// an event its forward transform waits for (its input's host copy) and one recorded after its back transform.
+fks_status fast_collision_pipelined(Ctx& c, const std::vector<PipeChunk>& ck, long long cap, cudaStream_t st) {
+  using namespace f32;
+  cudaError_t e = cudaSuccess;
+  if (!c.hot_stream) {
+    int lo = 0, hi = 0;
+    e = cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&c.hot_stream, cudaStreamNonBlocking, hi);
+    if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&c.side_stream, cudaStreamNonBlocking, lo);
+    for (int i = 0; i < 6 && e == cudaSuccess; i++) e = cudaEventCreateWithFlags(&c.ev_pipe[i], cudaEventDisableTiming);
+    if (e != cudaSuccess) { cudaGetLastError(); return cuda_status(e, "pipeline streams"); }
+  }
+  bool mom = false;
+  for (const PipeChunk& k : ck) mom = mom || k.U || k.W;
+  if (mom) {
+    fks_status rc = ensure_mpart(c, cap);
+    if (rc) return rc;
+  }
+  cudaStream_t hs = c.hot_stream, ss = c.side_stream;
+  cudaEvent_t ev_start = c.ev_pipe[0], ev_end = c.ev_pipe[5];
+  cudaEvent_t* ev_f = c.ev_pipe + 1;
+  cudaEvent_t* ev_h = c.ev_pipe + 3;
+  const size_t slot_bytes = fast_ws_bytes_per_cell(c) * (size_t)cap;
+  Slot sl[2] = {slot_at(c.d_ws, cap), slot_at(static_cast<char*>(c.d_ws) + slot_bytes, cap)};
+  const long long nc = (long long)ck.size();
+  auto fwd = [&](long long k) {
+    const PipeChunk& q = ck[k];
+    cudaError_t r = q.wait_before ? cudaStreamWaitEvent(ss, q.wait_before, 0) : cudaSuccess;
+    if (r != cudaSuccess) return r;
+    c.prof.begin(1, ss);
+    xform32_forward(c, q.fin, sl[k & 1].fhT, sl[k & 1].scratch, q.n, c.fast_variant, ss, q.has_g ? &q.g : nullptr);
+    c.prof.end(1, ss);
+    return cudaEventRecord(ev_f[k & 1], ss);
+  };
+  e = cudaEventRecord(ev_start, st);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(ss, ev_start, 0);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(hs, ev_start, 0);
+  if (e == cudaSuccess) e = fwd(0);
+  if (e == cudaSuccess && nc > 1) e = fwd(1);
+  for (long long k = 0; k < nc && e == cudaSuccess; k++) {
+    const PipeChunk& q = ck[k];
+    e = cudaStreamWaitEvent(hs, ev_f[k & 1], 0);
+    if (e != cudaSuccess) break;
+    c.prof.begin(2, hs);
+    fks_status rc = hot_launch(c, sl[k & 1], q.n, hs);
+    c.prof.end(2, hs);
+    if (rc) return rc;
+    e = cudaEventRecord(ev_h[k & 1], hs);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(ss, ev_h[k & 1], 0);
+    if (e != cudaSuccess) break;
+    c.prof.begin(3, ss);
+    back_chunk(c, sl[k & 1], q.fin, q.out, q.n, q.euler, q.s, ss, q.has_g ? &q.g : nullptr, q.U, q.W);
+    c.prof.end(3, ss);
+    if (q.record_after) e = cudaEventRecord(q.record_after, ss);
+    if (e == cudaSuccess && k + 2 < nc) e = fwd(k + 2);
+  }
+  // the side stream's last work (back(nc-1)) follows the last term-loop launch
+  if (e == cudaSuccess) e = cudaEventRecord(ev_end, ss);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(st, ev_end, 0);
+  if (e != cudaSuccess) { cudaGetLastError(); return cuda_status(e, "collision pipeline"); }
+  return cuda_status(cudaPeekAtLastError(), "fast collision pipeline");
 }
 
 }  // namespace fks

@@ -83,6 +83,12 @@ struct Ctx {
   bool slab_shift_valid = false;
   double* d_mpart = nullptr;            // fks_step_moments: per-CTA partial moment sums of the last kernel
   size_t mpart_elems = 0;
+  // N = 32 chunk pipeline (fast_collision_pipelined): the term-loop kernel of chunk k on a high-priority stream,
+  // the forward transform of chunk k+1 and the back transform of chunk k-1 on a low-priority stream, so that they
+  // run on the SMs the 12-CTA teams leave idle (148 = 12 x 12 + 4) and fill each launch's tail
+  cudaStream_t hot_stream = nullptr, side_stream = nullptr;
+  cudaEvent_t ev_pipe[6] = {};          // start, fwd[2], hot[2], end
+  bool pipeline = true;                 // FKS_NO_PIPELINE=1 turns it off (A/B)
 };
 
 // error plumbing
@@ -122,6 +128,21 @@ fks_status fast_collision(Ctx& c, const double* fin, double* out, long long n_ce
                           cudaStream_t st, const GatherSrc* gs = nullptr, double* U = nullptr, double* W = nullptr);
 size_t fast_ws_bytes_per_cell(const Ctx& c);
 fks_status fast_prepare(Ctx& c);
+// N = 32 only: chunks of at most `cap` cells through two workspace slots (the workspace holds 2 cap cells), the
+// three phases of consecutive chunks overlapped across streams; all work is ordered after st on entry and st waits
+// for all of it on return
+struct PipeChunk {
+  const double* fin;           // input cells (nullptr with a gather source)
+  double* out;
+  long long n;
+  bool euler; double s;
+  bool has_g; GatherSrc g;     // transport fused into the first and last kernels
+  double* U; double* W;        // optional moments of `out` ([n][5])
+  cudaEvent_t wait_before;     // optional: the chunk's forward transform waits for it (e.g. its input's H2D copy)
+  cudaEvent_t record_after;    // optional: recorded after the chunk's back transform (e.g. for its D2H copy)
+};
+bool fast_pipeline_ok(const Ctx& c);
+fks_status fast_collision_pipelined(Ctx& c, const std::vector<PipeChunk>& chunks, long long cap, cudaStream_t st);
 
 // small-N fast path (small.cu): N = 16 / 24 with P = 3N/2; generic forward / back transforms around one
 // persistent term-loop kernel (one CTA per (cell, z-class, term chunk) unit)

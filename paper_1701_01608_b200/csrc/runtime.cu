@@ -156,6 +156,26 @@ static fks_status run_collision(Ctx& c, const double* fin, double* out, long lon
   const bool fast = c.path == FKS_PATH_FAST;
   size_t per_cell = fast ? fast_ws_bytes_per_cell(c) : generic_ws_bytes_per_cell(c);
   long long ch = chunk_cells(c, per_cell, n);
+  if (fast && ch < n && fast_pipeline_ok(c)) {
+    // more than one chunk on the N = 32 path: two workspace slots, the chunks' phases overlapped across streams
+    // (the second slot is allocated only when the batch needs it)
+    fks_status rc = ensure_ws(c, 2 * per_cell * (size_t)ch);
+    if (rc) return rc;
+    const size_t nv = (size_t)c.N * c.N * c.N;
+    std::vector<PipeChunk> ck;
+    for (long long c0 = 0; c0 < n; c0 += ch) {
+      PipeChunk q{};
+      q.fin = gs ? nullptr : fin + c0 * nv;
+      q.out = out + c0 * nv;
+      q.n = std::min(ch, n - c0);
+      q.euler = euler; q.s = s;
+      if (gs) { q.has_g = true; q.g = *gs; q.g.cell0 = gs->cell0 + c0; }
+      q.U = U ? U + 5 * c0 : nullptr;
+      q.W = W ? W + 5 * c0 : nullptr;
+      ck.push_back(q);
+    }
+    return fast_collision_pipelined(c, ck, ch, st);
+  }
   fks_status rc = ensure_ws(c, per_cell * (size_t)ch);
   if (rc) return rc;
   const size_t nv = (size_t)c.N * c.N * c.N;
@@ -660,10 +680,45 @@ fks_status fks_step_host(fks_ctx* h, const double* f_in_host, double* f_out_host
     if (!rc) rc = cuda_status(cudaEventRecord(eh[i], c.h2d_stream), "event");
   }
   const bool ident = shift_is_identity(sh);
-  for (int i = 0; i < nk && !rc; i++) {
+  auto first_cell = [&](const Chunk& k) { return ((long long)k.xa * ny + k.ya) * c.nz; };
+  auto cells_of = [&](const Chunk& k) {
+    return (k.xb - k.xa == 1) ? (long long)(k.yb - k.ya) * c.nz : (long long)(k.xb - k.xa) * plane;
+  };
+  // N = 32: the pieces run through the chunk pipeline (forward / back transforms of neighbouring pieces beside
+  // the term loop, fast_collision_pipelined), each piece's forward transform waiting for its own copy-in and its
+  // copy-out waiting for its back transform
+  const bool fused = c.path == FKS_PATH_FAST && !std::getenv("FKS_UNFUSED_TRANSPORT");
+  long long cap = 0;
+  for (const Chunk& k : ch) cap = std::max(cap, cells_of(k));
+  const size_t pc_bytes = c.path == FKS_PATH_FAST ? fast_ws_bytes_per_cell(c) : 0;
+  const bool piped = !rc && nk >= 2 && fused && fast_pipeline_ok(c) && chunk_cells(c, pc_bytes, cap) >= cap;
+  if (piped) {
+    rc = ensure_ws(c, 2 * pc_bytes * (size_t)cap);
+    std::vector<PipeChunk> pc;
+    for (int i = 0; i < nk && !rc; i++) {
+      const long long c0 = first_cell(ch[i]);
+      PipeChunk q{};
+      q.fin = ident ? c.d_stage_in + c0 * nv : nullptr;
+      q.out = c.d_stage_out + c0 * nv;
+      q.n = cells_of(ch[i]);
+      q.euler = true; q.s = coll_scale;
+      if (!ident) { q.has_g = true; q.g = make_gather(c.d_stage_in, sh, c0); }
+      q.wait_before = eh[i];
+      q.record_after = ec[i];
+      pc.push_back(q);
+    }
+    if (!rc) rc = fast_collision_pipelined(c, pc, cap, st);
+    for (int i = 0; i < nk && !rc; i++) {
+      const long long c0 = first_cell(ch[i]), m = cells_of(ch[i]);
+      rc = cuda_status(cudaStreamWaitEvent(c.d2h_stream, ec[i], 0), "wait compute");
+      if (!rc) rc = cuda_status(cudaMemcpyAsync(f_out_host + c0 * nv, c.d_stage_out + c0 * nv, (size_t)m * nv * sizeof(double),
+                                                cudaMemcpyDeviceToHost, c.d2h_stream), "D2H");
+    }
+  }
+  for (int i = 0; i < nk && !rc && !piped; i++) {
     const Chunk& k = ch[i];
-    const long long c0 = ((long long)k.xa * ny + k.ya) * c.nz;
-    const long long m = (k.xb - k.xa == 1) ? (long long)(k.yb - k.ya) * c.nz : (long long)(k.xb - k.xa) * plane;
+    const long long c0 = first_cell(k);
+    const long long m = cells_of(k);
     rc = cuda_status(cudaStreamWaitEvent(st, eh[i], 0), "wait H2D");
     if (!rc) {
       if (ident) rc = run_collision(c, c.d_stage_in + c0 * nv, c.d_stage_out + c0 * nv, m, true, coll_scale, st);
@@ -873,6 +928,10 @@ void fks_destroy(fks_ctx* h) {
   if (c->stage_stream) cudaStreamDestroy(c->stage_stream);
   if (c->h2d_stream) cudaStreamDestroy(c->h2d_stream);
   if (c->d2h_stream) cudaStreamDestroy(c->d2h_stream);
+  if (c->hot_stream) cudaStreamDestroy(c->hot_stream);
+  if (c->side_stream) cudaStreamDestroy(c->side_stream);
+  for (cudaEvent_t ev : c->ev_pipe)
+    if (ev) cudaEventDestroy(ev);
   if (c->ev_done) cudaEventDestroy(c->ev_done);
   for (int ph = 0; ph < 4; ph++)
     for (auto& ev : c->prof.used[ph]) c->prof.pool.push_back(ev);

@@ -198,6 +198,32 @@ def test_chunking_matches_unchunked(cuda_device):
     assert torch.equal(q1, q2)
 
 
+@pytest.mark.parametrize("n, chunk", [(30, 7), (25, 12), (13, 12)])
+def test_pipelined_chunks_match_unchunked(cuda_device, monkeypatch, n, chunk):
+    """N = 32 batches of more than one workspace chunk run through the two-slot stream pipeline (the transforms of
+    chunks k - 1 and k + 1 beside the term loop of chunk k, fast32.cu fast_collision_pipelined): bit-identical to
+    one chunk and to the same chunking run sequentially (FKS_NO_PIPELINE=1 at init), for ragged last chunks,
+    two chunks and many; collision batch and Euler step with the fused transport gather."""
+    cfg = CONFIGS["c3"]
+    f = inputs.make_f(cfg, device=cuda_device, cells=list(range(n)))
+    whole = make(cfg)
+    piped = make(cfg, max_cells_in_flight=chunk)
+    monkeypatch.setenv("FKS_NO_PIPELINE", "1")
+    seq = make(cfg, max_cells_in_flight=chunk)
+    monkeypatch.delenv("FKS_NO_PIPELINE")
+    q = [c.collision_batch(f) for c in (whole, piped, seq)]
+    assert torch.equal(q[0], q[1]) and torch.equal(q[0], q[2])
+    shape = (n, 1, 1)
+    outs = []
+    for c in (whole, piped, seq):
+        c.transport_setup(shape, 1, 1)
+        out = torch.empty_like(f)
+        c.step(f, out, 0.05)
+        outs.append(out)
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])
+
+
 # ---------------- transport and the step ---------------------------------------------------------------
 
 def test_transport_bit_exact(cuda_device):
