@@ -578,7 +578,34 @@ fks_status fks_collision_batch_host(fks_ctx* h, const double* f_host, double* Q_
                                      cudaMemcpyHostToDevice, c.h2d_stream), "H2D");
     if (!rc) rc = cuda_status(cudaEventRecord(eh[i], c.h2d_stream), "event");
   }
-  for (long long i = 0; i < nch && !rc; i++) {
+  // N = 32: the chunks run through the chunk pipeline (each chunk's forward transform waits for its copy-in, its
+  // copy-out for its back transform), as in fks_step_host
+  const long long cap = (n_cells + nch - 1) / nch;
+  const size_t pc_bytes = c.path == FKS_PATH_FAST ? fast_ws_bytes_per_cell(c) : 0;
+  const bool piped = !rc && nch >= 2 && c.path == FKS_PATH_FAST && fast_pipeline_ok(c) &&
+                     chunk_cells(c, pc_bytes, cap) >= cap;
+  if (piped) {
+    rc = ensure_ws(c, 2 * pc_bytes * (size_t)cap);
+    std::vector<PipeChunk> pc;
+    for (long long i = 0; i < nch; i++) {
+      const long long c0 = n_cells * i / nch, m = n_cells * (i + 1) / nch - c0;
+      PipeChunk q{};
+      q.fin = c.d_stage_in + c0 * nv;
+      q.out = c.d_stage_out + c0 * nv;
+      q.n = m;
+      q.wait_before = eh[i];
+      q.record_after = ec[i];
+      pc.push_back(q);
+    }
+    if (!rc) rc = fast_collision_pipelined(c, pc, cap, st);
+    for (long long i = 0; i < nch && !rc; i++) {
+      const long long c0 = n_cells * i / nch, m = n_cells * (i + 1) / nch - c0;
+      rc = cuda_status(cudaStreamWaitEvent(c.d2h_stream, ec[i], 0), "wait compute");
+      if (!rc) rc = cuda_status(cudaMemcpyAsync(Q_host + c0 * nv, c.d_stage_out + c0 * nv, (size_t)m * nv * sizeof(double),
+                                                cudaMemcpyDeviceToHost, c.d2h_stream), "D2H");
+    }
+  }
+  for (long long i = 0; i < nch && !rc && !piped; i++) {
     const long long c0 = n_cells * i / nch, m = n_cells * (i + 1) / nch - c0;
     rc = cuda_status(cudaStreamWaitEvent(st, eh[i], 0), "wait H2D");
     if (!rc) rc = run_collision(c, c.d_stage_in + c0 * nv, c.d_stage_out + c0 * nv, m, false, 0.0, st);
