@@ -19,6 +19,7 @@
 // pinned to the TMEM lane quarter that holds their G block, the other tasks fill the least-loaded warps.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 #include "fks_internal.cuh"
@@ -557,11 +558,13 @@ fks_status small_prepare(Ctx& c) { return c.N == 16 ? small_prepare_n<16>(c) : s
 
 // term chunks per (cell, r): a function of N and the term count only (at most small_smax()), so that the
 // summation order of G — hence every bit of Q — does not depend on how a batch is split into calls or chunks
-// Chunks of ~32 terms at N = 24 (c1: 9 chunks, 1728 units = 11.7 waves of the 148-CTA grid; 1.5 % faster than
-// 16 chunks and half the partial-G traffic), ~8 terms at N = 16 (c0 has only 8 cells: parallelism over terms).
+// Chunks of ~26 terms at N = 24 (c1: 10 chunks, 1920 units = 12.97 waves of the 148-CTA grid, so the last wave is
+// full: 3.672 ms per c1 step vs 3.729 with 32-term chunks (11.7 waves), 3.722 with 20 and 3.818 with 16;
+// profiles/r02_experiments.txt r2sc), ~8 terms at N = 16 (c0 has only 8 cells: parallelism over terms).
 static int small_chunks(const Ctx& c) {
   const int T1 = c.T + 1;
-  const int tpc = c.N == 24 ? 32 : 8;
+  static const int tpc_env = [] { const char* e = std::getenv("FKS_SMALL_TPC"); return e ? std::atoi(e) : 0; }();
+  const int tpc = tpc_env > 0 ? tpc_env : (c.N == 24 ? 26 : 8);
   return std::max(1, std::min(small_smax(), (T1 + tpc - 1) / tpc));
 }
 
