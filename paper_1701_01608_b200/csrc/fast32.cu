@@ -693,10 +693,28 @@ fks_status fast_collision_pipelined(Ctx& c, const std::vector<PipeChunk>& ck, lo
   if (!c.hot_stream) {
     int lo = 0, hi = 0;
     e = cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    if (std::getenv("FKS_PIPE_NOPRIO")) hi = lo;  // experiment: both streams at the default priority
     if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&c.hot_stream, cudaStreamNonBlocking, hi);
     if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&c.side_stream, cudaStreamNonBlocking, lo);
     for (int i = 0; i < 6 && e == cudaSuccess; i++) e = cudaEventCreateWithFlags(&c.ev_pipe[i], cudaEventDisableTiming);
     if (e != cudaSuccess) { cudaGetLastError(); return cuda_status(e, "pipeline streams"); }
+    if (std::getenv("FKS_L2_PERSIST")) {  // experiment: keep the W1 ring L2-resident against the side streams
+      int maxwin = 0, maxpers = 0;
+      cudaDeviceGetAttribute(&maxwin, cudaDevAttrMaxAccessPolicyWindowSize, c.device);
+      cudaDeviceGetAttribute(&maxpers, cudaDevAttrMaxPersistingL2CacheSize, c.device);
+      const size_t w1b = (size_t)c.fast_nteams * v4::NB * W1_BUF * sizeof(double2);
+      const size_t win = std::min<size_t>(w1b, (size_t)maxwin);
+      cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min<size_t>(win, (size_t)maxpers));
+      cudaStreamAttrValue av{};
+      av.accessPolicyWindow.base_ptr = c.d_w1;
+      av.accessPolicyWindow.num_bytes = win;
+      av.accessPolicyWindow.hitRatio = 1.0f;
+      av.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+      av.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+      cudaStreamSetAttribute(c.hot_stream, cudaStreamAttributeAccessPolicyWindow, &av);
+      cudaGetLastError();
+      fprintf(stderr, "FKS_L2_PERSIST: window %zu of %zu B, persisting limit %d, max window %d\n", win, w1b, maxpers, maxwin);
+    }
   }
   bool mom = false;
   for (const PipeChunk& k : ck) mom = mom || k.U || k.W;
