@@ -589,7 +589,8 @@ fks_status fast_prepare(Ctx& c) {
   c.pipeline = std::getenv("FKS_NO_PIPELINE") == nullptr;
   c.fast_nteams = c.num_sms / v4::TM;
   if (c.fast_nteams < 1) { set_error("fewer SMs than one team"); return FKS_ERR_UNSUPPORTED; }
-  e = cudaMalloc(&c.d_ctr, (size_t)c.fast_nteams * v4::CTR_STRIDE * sizeof(unsigned));
+  // two counter sets: the chunk pipeline zeroes the set of launch k + 2 on the side stream while launch k + 1 runs
+  e = cudaMalloc(&c.d_ctr, 2 * (size_t)c.fast_nteams * v4::CTR_STRIDE * sizeof(unsigned));
   if (e != cudaSuccess) { cudaGetLastError(); return cuda_status(e, "team counters"); }
   const size_t w1_elems = (size_t)c.fast_nteams * v4::NB * W1_BUF;
   const size_t n = (size_t)(c.T + 1) * LHN;
@@ -616,11 +617,16 @@ Slot slot_at(void* base, long long cap) {
   return sl;
 }
 
-fks_status hot_launch(Ctx& c, const Slot& sl, long long n, cudaStream_t st) {
+size_t ctr_set_bytes(const Ctx& c) { return (size_t)c.fast_nteams * f32::v4::CTR_STRIDE * sizeof(unsigned); }
+
+// term-loop launch over the counter set `set`; zero_ctr: zero the set on `st` first (the pipeline zeroes it ahead on
+// the side stream, so that nothing but the launch itself sits between two term-loop launches on the hot stream)
+fks_status hot_launch(Ctx& c, const Slot& sl, long long n, cudaStream_t st, int set = 0, bool zero_ctr = true) {
   using namespace f32;
   const long long nt = std::min<long long>(c.fast_nteams, n);
-  v4::Args A{sl.fhT, c.d_abT, sl.G, c.d_w1, c.d_ctr, n, c.T + 1, (int)nt, c.dbg};
-  cudaMemsetAsync(c.d_ctr, 0, (size_t)c.fast_nteams * v4::CTR_STRIDE * sizeof(unsigned), st);
+  unsigned* ctr = c.d_ctr + (size_t)set * (ctr_set_bytes(c) / sizeof(unsigned));
+  v4::Args A{sl.fhT, c.d_abT, sl.G, c.d_w1, ctr, n, c.T + 1, (int)nt, c.dbg};
+  if (zero_ctr) cudaMemsetAsync(ctr, 0, ctr_set_bytes(c), st);
   void* args[] = {&A};
   // cooperative launch: the teams spin on each other's counters, so every CTA must be co-resident
   cudaError_t e = cudaLaunchCooperativeKernel((void*)v4::hot_kernel_v4, dim3((unsigned)(nt * v4::TM)),
@@ -738,9 +744,11 @@ fks_status fast_collision_pipelined(Ctx& c, const std::vector<PipeChunk>& ck, lo
     c.prof.end(1, ss);
     return cudaEventRecord(ev_f[k & 1], ss);
   };
+  const bool ctr_ahead = std::getenv("FKS_PIPE_HOT_MEMSET") == nullptr;
   e = cudaEventRecord(ev_start, st);
   if (e == cudaSuccess) e = cudaStreamWaitEvent(ss, ev_start, 0);
   if (e == cudaSuccess) e = cudaStreamWaitEvent(hs, ev_start, 0);
+  if (e == cudaSuccess && ctr_ahead) e = cudaMemsetAsync(c.d_ctr, 0, 2 * ctr_set_bytes(c), ss);
   if (e == cudaSuccess) e = fwd(0);
   if (e == cudaSuccess && nc > 1) e = fwd(1);
   for (long long k = 0; k < nc && e == cudaSuccess; k++) {
@@ -748,7 +756,7 @@ fks_status fast_collision_pipelined(Ctx& c, const std::vector<PipeChunk>& ck, lo
     e = cudaStreamWaitEvent(hs, ev_f[k & 1], 0);
     if (e != cudaSuccess) break;
     c.prof.begin(2, hs);
-    fks_status rc = hot_launch(c, sl[k & 1], q.n, hs);
+    fks_status rc = hot_launch(c, sl[k & 1], q.n, hs, (int)(k & 1), !ctr_ahead);
     c.prof.end(2, hs);
     if (rc) return rc;
     e = cudaEventRecord(ev_h[k & 1], hs);
@@ -758,6 +766,9 @@ fks_status fast_collision_pipelined(Ctx& c, const std::vector<PipeChunk>& ck, lo
     back_chunk(c, sl[k & 1], q.fin, q.out, q.n, q.euler, q.s, ss, q.has_g ? &q.g : nullptr, q.U, q.W);
     c.prof.end(3, ss);
     if (q.record_after) e = cudaEventRecord(q.record_after, ss);
+    // counter set k % 2 is free (launch k is done: back k waited for it); launch k + 2 waits for fwd(k + 2) below
+    if (e == cudaSuccess && ctr_ahead && k + 2 < nc)
+      e = cudaMemsetAsync(c.d_ctr + (size_t)(k & 1) * (ctr_set_bytes(c) / sizeof(unsigned)), 0, ctr_set_bytes(c), ss);
     if (e == cudaSuccess && k + 2 < nc) e = fwd(k + 2);
   }
   // the side stream's last work (back(nc-1)) follows the last term-loop launch
