@@ -664,11 +664,24 @@ fks_status fks_step_host(fks_ctx* h, const double* f_in_host, double* f_out_host
   // slab, when they are one plane of >= 16 rows, are cut into 4 row blocks: the first computation then waits only
   // for the rows it reads (its plane and its x-neighbours, its rows +- max|delta_y|) and the last copy-out is a
   // quarter plane (round 2: about 14 ms less exposed copy per c3 step).
+  // A first / last slab of several planes (a slab box such as c2: 512 x 1 x 1) gives up its outer quarter (at least
+  // max|delta_x| planes) as a piece of its own, for the same reason: less copy exposed at the two ends.
   struct Chunk { int xa, xb, ya, yb; };
-  std::vector<Chunk> ch;
+  std::vector<std::pair<int, int>> xs;
+  const int wmin = std::max(1, dmax);
   for (int i = 0; i < nch; i++) {
     const int xa = (int)((long long)nx * i / nch), xb = (int)((long long)nx * (i + 1) / nch);
-    const bool split = nch > 1 && (i == 0 || i == nch - 1) && xb - xa == 1 && ny >= 16 && ny >= 4 * (2 * dmy + 1);
+    const bool carve = nch >= 3 && (i == 0 || i == nch - 1) && xb - xa >= 4 * wmin && !std::getenv("FKS_HOST_NO_CARVE");
+    if (!carve) { xs.push_back({xa, xb}); continue; }
+    const int w = std::max(wmin, (xb - xa) / 4);
+    if (i == 0) { xs.push_back({xa, xa + w}); xs.push_back({xa + w, xb}); }
+    else { xs.push_back({xa, xb - w}); xs.push_back({xb - w, xb}); }
+  }
+  std::vector<Chunk> ch;
+  const int nxs = (int)xs.size();
+  for (int i = 0; i < nxs; i++) {
+    const int xa = xs[i].first, xb = xs[i].second;
+    const bool split = nxs > 1 && (i == 0 || i == nxs - 1) && xb - xa == 1 && ny >= 16 && ny >= 4 * (2 * dmy + 1);
     const int parts = split ? 4 : 1;
     for (int q = 0; q < parts; q++) ch.push_back({xa, xb, (int)((long long)ny * q / parts), (int)((long long)ny * (q + 1) / parts)});
   }

@@ -412,11 +412,14 @@ def test_step_host_matches_device(cuda_device, name, shape, cfl):
 
 
 @pytest.mark.parametrize("name,shape,cfl,slabs", [("c0", (4, 16, 2), (1, 1), "4"), ("c0", (6, 16, 1), (3, 2), "6"),
-                                                   ("c2", (4, 16, 1), (1, 1), "4")])
+                                                   ("c2", (4, 16, 1), (1, 1), "4"), ("c2", (64, 1, 1), (1, 1), "4"),
+                                                   ("c2", (48, 1, 1), (3, 1), "3")])
 def test_step_host_split_slabs(cuda_device, monkeypatch, name, shape, cfl, slabs):
     """fks_step_host with one-plane slabs whose first and last plane are cut into 4 row blocks (each copied and
-    computed as soon as the rows it reads have landed, y-halo of max|delta_y| rows, periodic in y): bit-identical
-    to fks_step over two steps, on the small-N path (c0) and the N = 32 fast path (c2 cells, fused gather)."""
+    computed as soon as the rows it reads have landed, y-halo of max|delta_y| rows, periodic in y), and with
+    multi-plane slabs whose first and last slab give up their outer quarter (>= max|delta_x| planes) as a piece of
+    its own (c2-like 1-D boxes, CFL 1 and 3): bit-identical to fks_step over two steps, on the small-N path (c0)
+    and the N = 32 fast path (c2 cells, fused gather, chunk pipeline)."""
     monkeypatch.setenv("FKS_HOST_SLABS", slabs)
     test_step_host_matches_device(cuda_device, name, shape, cfl)
 

@@ -29,8 +29,13 @@ def make(cfg, **kw):
     return B.Collision(cfg.N, cfg.L, cfg.M, cfg.M_r, cfg.kernel, **kw)
 
 
-def team_blocks(n_cells: int, width: int = 12):
-    starts = sorted({0, max(0, n_cells // 2 - width // 2), max(0, n_cells - width)})
+def team_blocks(n_cells: int, width: int = 12, nblocks: int = 3):
+    """Blocks of `width` consecutive cells (every team of a chunk) at nblocks evenly spaced starts, first and last
+    cells included."""
+    if nblocks == 3:
+        starts = sorted({0, max(0, n_cells // 2 - width // 2), max(0, n_cells - width)})
+    else:
+        starts = sorted({min(max(0, n_cells - width), (n_cells - width) * i // (nblocks - 1)) for i in range(nblocks)})
     return sorted({c for s in starts for c in range(s, min(n_cells, s + width))})
 
 
@@ -103,7 +108,8 @@ def test_step_c1_homogeneous_all_cells(cuda_device):
 
 
 def test_step_c4_two_steps_dense_sample(cuda_device):
-    """c4 (48³ cells, M = 64, c = 1/8, Kn = 0.01) at full size: two steps, 36 cells per step."""
+    """c4 (48³ cells, M = 64, c = 1/8, Kn = 0.01) at full size: two steps, 12 blocks of 12 cells per step, so that
+    every workspace chunk (about 11 per step) and both slots of the chunk pipeline are sampled."""
     cfg = CONFIGS["c4"]
     f = inputs.make_f(cfg, device=cuda_device)
     g = torch.empty_like(f)
@@ -116,7 +122,7 @@ def test_step_c4_two_steps_dense_sample(cuda_device):
         col.step(cur, nxt, cfg.coll_scale)
         torch.cuda.synchronize()
         d = cell.advance()
-        check_step_cells(cur, nxt, team_blocks(cfg.n_cells), cfg.shape, d, tb, cfg.coll_scale)
+        check_step_cells(cur, nxt, team_blocks(cfg.n_cells, nblocks=12), cfg.shape, d, tb, cfg.coll_scale)
         cur, nxt = nxt, cur
     del f, g
 
