@@ -564,7 +564,21 @@ fks_status fks_collision_batch_host(fks_ctx* h, const double* f_host, double* Q_
   if (!c.h2d_stream) cudaStreamCreateWithFlags(&c.h2d_stream, cudaStreamNonBlocking);
   if (!c.d2h_stream) cudaStreamCreateWithFlags(&c.d2h_stream, cudaStreamNonBlocking);
   const long long nv = (long long)c.N * c.N * c.N;
-  const long long nch = std::max(1LL, std::min(32LL, n_cells / 512));
+  // chunks of >= 32 MB of input (at most 32), the first and the last one with their outer quarter cut off as a
+  // chunk of its own, so that only a small copy-in and copy-out stay exposed at the two ends (c2: 512 cells of
+  // 256 KB -> 4 chunks + 2 quarter chunks; it was one chunk with both copies exposed)
+  std::vector<long long> cb;  // chunk boundaries
+  {
+    const long long box_bytes = n_cells * nv * (long long)sizeof(double);
+    const long long n0 = std::max(1LL, std::min({32LL, box_bytes / (32LL << 20), n_cells}));
+    for (long long i = 0; i <= n0; i++) cb.push_back(n_cells * i / n0);
+    if (n0 >= 3 && cb[1] - cb[0] >= 4 && !std::getenv("FKS_HOST_NO_CARVE")) {
+      cb.insert(cb.begin() + 1, cb[0] + (cb[1] - cb[0]) / 4);
+      const size_t e = cb.size() - 1;
+      cb.insert(cb.begin() + e, cb[e] - (cb[e] - cb[e - 1]) / 4);
+    }
+  }
+  const long long nch = (long long)cb.size() - 1;
   cudaStream_t st = c.stage_stream;
   if ((rc = order_begin(c, st)) || (rc = order_begin(c, c.h2d_stream))) return rc;
   std::vector<cudaEvent_t> eh(nch), ec(nch);
@@ -573,14 +587,15 @@ fks_status fks_collision_batch_host(fks_ctx* h, const double* f_host, double* Q_
     cudaEventCreateWithFlags(&ec[i], cudaEventDisableTiming);
   }
   for (long long i = 0; i < nch && !rc; i++) {
-    const long long c0 = n_cells * i / nch, m = n_cells * (i + 1) / nch - c0;
+    const long long c0 = cb[i], m = cb[i + 1] - cb[i];
     rc = cuda_status(cudaMemcpyAsync(c.d_stage_in + c0 * nv, f_host + c0 * nv, (size_t)m * nv * sizeof(double),
                                      cudaMemcpyHostToDevice, c.h2d_stream), "H2D");
     if (!rc) rc = cuda_status(cudaEventRecord(eh[i], c.h2d_stream), "event");
   }
   // N = 32: the chunks run through the chunk pipeline (each chunk's forward transform waits for its copy-in, its
   // copy-out for its back transform), as in fks_step_host
-  const long long cap = (n_cells + nch - 1) / nch;
+  long long cap = 0;
+  for (long long i = 0; i < nch; i++) cap = std::max(cap, cb[i + 1] - cb[i]);
   const size_t pc_bytes = c.path == FKS_PATH_FAST ? fast_ws_bytes_per_cell(c) : 0;
   const bool piped = !rc && nch >= 2 && c.path == FKS_PATH_FAST && fast_pipeline_ok(c) &&
                      chunk_cells(c, pc_bytes, cap) >= cap;
@@ -588,7 +603,7 @@ fks_status fks_collision_batch_host(fks_ctx* h, const double* f_host, double* Q_
     rc = ensure_ws(c, 2 * pc_bytes * (size_t)cap);
     std::vector<PipeChunk> pc;
     for (long long i = 0; i < nch; i++) {
-      const long long c0 = n_cells * i / nch, m = n_cells * (i + 1) / nch - c0;
+      const long long c0 = cb[i], m = cb[i + 1] - cb[i];
       PipeChunk q{};
       q.fin = c.d_stage_in + c0 * nv;
       q.out = c.d_stage_out + c0 * nv;
@@ -599,14 +614,14 @@ fks_status fks_collision_batch_host(fks_ctx* h, const double* f_host, double* Q_
     }
     if (!rc) rc = fast_collision_pipelined(c, pc, cap, st);
     for (long long i = 0; i < nch && !rc; i++) {
-      const long long c0 = n_cells * i / nch, m = n_cells * (i + 1) / nch - c0;
+      const long long c0 = cb[i], m = cb[i + 1] - cb[i];
       rc = cuda_status(cudaStreamWaitEvent(c.d2h_stream, ec[i], 0), "wait compute");
       if (!rc) rc = cuda_status(cudaMemcpyAsync(Q_host + c0 * nv, c.d_stage_out + c0 * nv, (size_t)m * nv * sizeof(double),
                                                 cudaMemcpyDeviceToHost, c.d2h_stream), "D2H");
     }
   }
   for (long long i = 0; i < nch && !rc && !piped; i++) {
-    const long long c0 = n_cells * i / nch, m = n_cells * (i + 1) / nch - c0;
+    const long long c0 = cb[i], m = cb[i + 1] - cb[i];
     rc = cuda_status(cudaStreamWaitEvent(st, eh[i], 0), "wait H2D");
     if (!rc) rc = run_collision(c, c.d_stage_in + c0 * nv, c.d_stage_out + c0 * nv, m, false, 0.0, st);
     if (!rc) rc = cuda_status(cudaEventRecord(ec[i], st), "event");

@@ -199,7 +199,10 @@ __global__ void __launch_bounds__(256, 3) kf2(const double2* __restrict__ F2, do
 // kb1: CTA = (cell, 4 px planes), 288 threads.  First axis (py, contiguous): two real rows packed as one
 // complex row, FFT48, untangled on the fly (ky = 0..15);  second axis (pz): FFT48 -> kz in K'.
 // Out H2[cell][px][kz][ky].
-__global__ void __launch_bounds__(KB1_T, 8 / PB1) kb1(const double* __restrict__ G, double2* __restrict__ H2) {
+#ifndef KB1_MINB
+#define KB1_MINB (8 / PB1)
+#endif
+__global__ void __launch_bounds__(KB1_T, KB1_MINB) kb1(const double* __restrict__ G, double2* __restrict__ H2) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   // [4 planes][24 row pairs][ZS]: element py of the pair = (G(pz = 2pr, py), G(pz = 2pr+1, py)); then in
   // place the complex FFT48 of the pair
