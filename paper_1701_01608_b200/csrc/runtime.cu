@@ -162,12 +162,27 @@ static fks_status run_collision(Ctx& c, const double* fin, double* out, long lon
     fks_status rc = ensure_ws(c, 2 * per_cell * (size_t)ch);
     if (rc) return rc;
     const size_t nv = (size_t)c.N * c.N * c.N;
+    // chunk boundaries: the first and the last chunk a quarter slot, so that the forward transform before the first
+    // term-loop launch and the back transform after the last one (the two the pipeline cannot hide) are short; the
+    // rest split evenly into full-slot-or-smaller chunks
+    std::vector<long long> cb{0};
+    const long long q4 = ch / 4;
+    if (n >= 2 * q4 + ch && q4 >= 1 && !std::getenv("FKS_PIPE_NO_CARVE")) {
+      cb.push_back(q4);
+      const long long mid = n - 2 * q4, nm = (mid + ch - 1) / ch;
+      for (long long i = 1; i <= nm; i++) cb.push_back(q4 + mid * i / nm);
+      cb.push_back(n);
+    } else {
+      for (long long c0 = ch; c0 < n; c0 += ch) cb.push_back(c0);
+      cb.push_back(n);
+    }
     std::vector<PipeChunk> ck;
-    for (long long c0 = 0; c0 < n; c0 += ch) {
+    for (size_t i = 0; i + 1 < cb.size(); i++) {
+      const long long c0 = cb[i];
       PipeChunk q{};
       q.fin = gs ? nullptr : fin + c0 * nv;
       q.out = out + c0 * nv;
-      q.n = std::min(ch, n - c0);
+      q.n = cb[i + 1] - c0;
       q.euler = euler; q.s = s;
       if (gs) { q.has_g = true; q.g = *gs; q.g.cell0 = gs->cell0 + c0; }
       q.U = U ? U + 5 * c0 : nullptr;
