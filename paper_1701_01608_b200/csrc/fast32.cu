@@ -745,6 +745,7 @@ fks_status fast_collision_pipelined(Ctx& c, const std::vector<PipeChunk>& ck, lo
     return cudaEventRecord(ev_f[k & 1], ss);
   };
   const bool ctr_ahead = std::getenv("FKS_PIPE_HOT_MEMSET") == nullptr;
+  fks_status hot_rc = FKS_OK;
   e = cudaEventRecord(ev_start, st);
   if (e == cudaSuccess) e = cudaStreamWaitEvent(ss, ev_start, 0);
   if (e == cudaSuccess) e = cudaStreamWaitEvent(hs, ev_start, 0);
@@ -758,7 +759,7 @@ fks_status fast_collision_pipelined(Ctx& c, const std::vector<PipeChunk>& ck, lo
     c.prof.begin(2, hs);
     fks_status rc = hot_launch(c, sl[k & 1], q.n, hs, (int)(k & 1), !ctr_ahead);
     c.prof.end(2, hs);
-    if (rc) return rc;
+    if (rc) { hot_rc = rc; break; }
     e = cudaEventRecord(ev_h[k & 1], hs);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(ss, ev_h[k & 1], 0);
     if (e != cudaSuccess) break;
@@ -771,10 +772,17 @@ fks_status fast_collision_pipelined(Ctx& c, const std::vector<PipeChunk>& ck, lo
       e = cudaMemsetAsync(c.d_ctr + (size_t)(k & 1) * (ctr_set_bytes(c) / sizeof(unsigned)), 0, ctr_set_bytes(c), ss);
     if (e == cudaSuccess && k + 2 < nc) e = fwd(k + 2);
   }
-  // the side stream's last work (back(nc-1)) follows the last term-loop launch
-  if (e == cudaSuccess) e = cudaEventRecord(ev_end, ss);
-  if (e == cudaSuccess) e = cudaStreamWaitEvent(st, ev_end, 0);
-  if (e != cudaSuccess) { cudaGetLastError(); return cuda_status(e, "collision pipeline"); }
+  // join: the side stream's last work (back(nc-1)) follows the last term-loop launch; st waits for both streams
+  // (also after an error part-way, so that no work enqueued here outlives the call's ordering on st)
+  const cudaError_t e_join = e;
+  if (e_join != cudaSuccess) cudaGetLastError();
+  cudaError_t ej = cudaEventRecord(ev_end, ss);
+  if (ej == cudaSuccess) ej = cudaStreamWaitEvent(st, ev_end, 0);
+  if (ej == cudaSuccess) ej = cudaEventRecord(ev_end, hs);
+  if (ej == cudaSuccess) ej = cudaStreamWaitEvent(st, ev_end, 0);
+  if (hot_rc) return hot_rc;
+  if (e_join != cudaSuccess) return cuda_status(e_join, "collision pipeline");
+  if (ej != cudaSuccess) { cudaGetLastError(); return cuda_status(ej, "collision pipeline join"); }
   return cuda_status(cudaPeekAtLastError(), "fast collision pipeline");
 }
 
