@@ -156,11 +156,9 @@ static fks_status run_collision(Ctx& c, const double* fin, double* out, long lon
   const bool fast = c.path == FKS_PATH_FAST;
   size_t per_cell = fast ? fast_ws_bytes_per_cell(c) : generic_ws_bytes_per_cell(c);
   long long ch = chunk_cells(c, per_cell, n);
-  if (fast && ch < n && fast_pipeline_ok(c)) {
-    // more than one chunk on the N = 32 path: two workspace slots, the chunks' phases overlapped across streams
-    // (the second slot is allocated only when the batch needs it)
-    fks_status rc = ensure_ws(c, 2 * per_cell * (size_t)ch);
-    if (rc) return rc;
+  // more than one chunk on the N = 32 path: two workspace slots, the chunks' phases overlapped across streams (the
+  // second slot is allocated only when the batch needs it; if it cannot be, the chunks run one after another)
+  if (fast && ch < n && fast_pipeline_ok(c) && ensure_ws(c, 2 * per_cell * (size_t)ch) == FKS_OK) {
     const size_t nv = (size_t)c.N * c.N * c.N;
     // chunk boundaries: the first and the last chunk a quarter slot, so that the forward transform before the first
     // term-loop launch and the back transform after the last one (the two the pipeline cannot hide) are short; the
@@ -613,9 +611,9 @@ fks_status fks_collision_batch_host(fks_ctx* h, const double* f_host, double* Q_
   for (long long i = 0; i < nch; i++) cap = std::max(cap, cb[i + 1] - cb[i]);
   const size_t pc_bytes = c.path == FKS_PATH_FAST ? fast_ws_bytes_per_cell(c) : 0;
   const bool piped = !rc && nch >= 2 && c.path == FKS_PATH_FAST && fast_pipeline_ok(c) &&
-                     chunk_cells(c, pc_bytes, cap) >= cap;
+                     chunk_cells(c, pc_bytes, cap) >= cap &&
+                     ensure_ws(c, 2 * pc_bytes * (size_t)cap) == FKS_OK;  // else the chunks run one by one
   if (piped) {
-    rc = ensure_ws(c, 2 * pc_bytes * (size_t)cap);
     std::vector<PipeChunk> pc;
     for (long long i = 0; i < nch; i++) {
       const long long c0 = cb[i], m = cb[i + 1] - cb[i];
@@ -761,9 +759,9 @@ fks_status fks_step_host(fks_ctx* h, const double* f_in_host, double* f_out_host
   long long cap = 0;
   for (const Chunk& k : ch) cap = std::max(cap, cells_of(k));
   const size_t pc_bytes = c.path == FKS_PATH_FAST ? fast_ws_bytes_per_cell(c) : 0;
-  const bool piped = !rc && nk >= 2 && fused && fast_pipeline_ok(c) && chunk_cells(c, pc_bytes, cap) >= cap;
+  const bool piped = !rc && nk >= 2 && fused && fast_pipeline_ok(c) && chunk_cells(c, pc_bytes, cap) >= cap &&
+                     ensure_ws(c, 2 * pc_bytes * (size_t)cap) == FKS_OK;  // else the pieces run one by one
   if (piped) {
-    rc = ensure_ws(c, 2 * pc_bytes * (size_t)cap);
     std::vector<PipeChunk> pc;
     for (int i = 0; i < nk && !rc; i++) {
       const long long c0 = first_cell(ch[i]);
