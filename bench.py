@@ -550,6 +550,12 @@ def main():
                      "kernel": ("term loop (a3-a5): " + ("hot_kernel_v4, 12-CTA teams" if cfg.N == 32 else
                                 "small_term_kernel, one CTA per (cell, z-class, term chunk)")),
                      "flop_per_cell": fl["hot"], "cells_per_launch": cells_per_launch, "ms_per_launch": hot_ms,
+                     "timing_note": ("CUDA events on the term-loop kernel's own (high-priority) stream, each launch "
+                                     "running beside the chunk pipeline's forward / back transforms on the SMs its "
+                                     "teams leave free (DESIGN.md §5); run alone it is ~0.5 % faster "
+                                     "(FKS_NO_PIPELINE=1)") if (cfg.N == 32 and ph_cnt[2] > args.steps
+                                                               and not os.environ.get("FKS_NO_PIPELINE"))
+                                    else "CUDA events on the launching stream",
                      "frac_of_measured_dfma": achieved / 36.66,
                      "peak_at_max_clock": fp64_peak_tflops(1965.0),
                      # the N = 32 kernel is sensitive to how its warp roles phase-lock; the shipped
