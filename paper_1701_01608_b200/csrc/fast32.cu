@@ -655,6 +655,34 @@ void back_chunk(Ctx& c, const Slot& sl, const double* fin, double* out, long lon
   xform32_back(c, sl.G, sl.scratch, sl.fhT, fin, out, n, euler, s, st, gs, mpart);
   if (mpart) launch_moments_finish(c, mpart, f32::N / 8, n, U, W, st);
 }
+
+// Cells [o, o + m) of a pipelined chunk: the transform kernels index their buffers cell-major, each with its own
+// per-cell stride (f / out N^3, F2 and E1 N K H, H2 P K H complex, f^ LHN complex, G P^3, moment partials (N/8) 5).
+void fwd_range(Ctx& c, const Slot& sl, const PipeChunk& q, long long o, long long m, cudaStream_t st) {
+  using namespace f32;
+  constexpr long long H = N / 2;
+  GatherSrc g = q.g;
+  if (q.has_g) g.cell0 += o;
+  xform32_forward(c, q.fin ? q.fin + o * (long long)N * N * N : nullptr, sl.fhT + o * LHN, sl.scratch + o * N * K * H,
+                  m, c.fast_variant, st, q.has_g ? &g : nullptr);
+}
+void back_range(Ctx& c, const Slot& sl, const PipeChunk& q, long long o, long long m, cudaStream_t st) {
+  using namespace f32;
+  constexpr long long H = N / 2, nv = (long long)N * N * N;
+  GatherSrc g = q.g;
+  if (q.has_g) g.cell0 += o;
+  double* mpart = (q.U || q.W) ? c.d_mpart + o * (N / 8) * 5 : nullptr;
+  xform32_back(c, sl.G + o * (long long)P * P * P, sl.scratch + o * P * K * H, sl.fhT + o * N * K * H,
+               q.fin ? q.fin + o * nv : nullptr, q.out + o * nv, m, q.euler, q.s, st, q.has_g ? &g : nullptr, mpart);
+  if (mpart) launch_moments_finish(c, mpart, N / 8, m, q.U ? q.U + 5 * o : nullptr, q.W ? q.W + 5 * o : nullptr, st);
+}
+// Side-stream kernels are launched over sub-ranges of at most this many cells: a term-loop launch that becomes ready
+// while a side kernel is running has to wait for SMs that side CTAs keep occupying until that kernel's grid is
+// dispatched, so short side grids bound the wait (FKS_PIPE_SUB cells; 0 = whole chunks)
+long long pipe_sub_cells() {
+  const char* e = std::getenv("FKS_PIPE_SUB");
+  return e ? std::atoll(e) : 1024LL;
+}
 }  // namespace
 
 fks_status fast_collision(Ctx& c, const double* fin, double* out, long long n, bool euler, double s,
@@ -735,12 +763,13 @@ fks_status fast_collision_pipelined(Ctx& c, const std::vector<PipeChunk>& ck, lo
   const size_t slot_bytes = fast_ws_bytes_per_cell(c) * (size_t)cap;
   Slot sl[2] = {slot_at(c.d_ws, cap), slot_at(static_cast<char*>(c.d_ws) + slot_bytes, cap)};
   const long long nc = (long long)ck.size();
+  const long long sub = pipe_sub_cells() > 0 ? pipe_sub_cells() : cap;
   auto fwd = [&](long long k) {
     const PipeChunk& q = ck[k];
     cudaError_t r = q.wait_before ? cudaStreamWaitEvent(ss, q.wait_before, 0) : cudaSuccess;
     if (r != cudaSuccess) return r;
     c.prof.begin(1, ss);
-    xform32_forward(c, q.fin, sl[k & 1].fhT, sl[k & 1].scratch, q.n, c.fast_variant, ss, q.has_g ? &q.g : nullptr);
+    for (long long o = 0; o < q.n; o += sub) fwd_range(c, sl[k & 1], q, o, std::min(sub, q.n - o), ss);
     c.prof.end(1, ss);
     return cudaEventRecord(ev_f[k & 1], ss);
   };
@@ -764,7 +793,7 @@ fks_status fast_collision_pipelined(Ctx& c, const std::vector<PipeChunk>& ck, lo
     if (e == cudaSuccess) e = cudaStreamWaitEvent(ss, ev_h[k & 1], 0);
     if (e != cudaSuccess) break;
     c.prof.begin(3, ss);
-    back_chunk(c, sl[k & 1], q.fin, q.out, q.n, q.euler, q.s, ss, q.has_g ? &q.g : nullptr, q.U, q.W);
+    for (long long o = 0; o < q.n; o += sub) back_range(c, sl[k & 1], q, o, std::min(sub, q.n - o), ss);
     c.prof.end(3, ss);
     if (q.record_after) e = cudaEventRecord(q.record_after, ss);
     // counter set k % 2 is free (launch k is done: back k waited for it); launch k + 2 waits for fwd(k + 2) below

@@ -288,9 +288,13 @@ def test_step_moments_argument_checks(cuda_device):
     assert ei.value.status == B.FKS_ERR_INVALID
 
 
-def test_step_moments_chunked(cuda_device):
+@pytest.mark.parametrize("sub", [None, "3"])
+def test_step_moments_chunked(cuda_device, monkeypatch, sub):
     """fks_step_moments when the step runs in several workspace chunks (max_cells_in_flight): the moment rows of
-    every chunk land at their cells' offsets (fast path, fused gather)."""
+    every chunk land at their cells' offsets (fast path, fused gather; chunk pipeline, also with its side-stream
+    transforms over sub-ranges of 3 cells, FKS_PIPE_SUB)."""
+    if sub is not None:
+        monkeypatch.setenv("FKS_PIPE_SUB", sub)
     N, shape = 32, (5, 2, 2)
     n = int(np.prod(shape))
     f = torch.as_tensor(_random_two_maxwellian(n, N, L_BOX, 404), device=cuda_device)

@@ -198,12 +198,15 @@ def test_chunking_matches_unchunked(cuda_device):
     assert torch.equal(q1, q2)
 
 
-@pytest.mark.parametrize("n, chunk", [(30, 7), (25, 12), (13, 12)])
-def test_pipelined_chunks_match_unchunked(cuda_device, monkeypatch, n, chunk):
+@pytest.mark.parametrize("n, chunk, sub", [(30, 7, None), (25, 12, None), (13, 12, None), (40, 16, "3"), (30, 12, "5")])
+def test_pipelined_chunks_match_unchunked(cuda_device, monkeypatch, n, chunk, sub):
     """N = 32 batches of more than one workspace chunk run through the two-slot stream pipeline (the transforms of
     chunks k - 1 and k + 1 beside the term loop of chunk k, fast32.cu fast_collision_pipelined): bit-identical to
     one chunk and to the same chunking run sequentially (FKS_NO_PIPELINE=1 at init), for ragged last chunks,
-    two chunks and many; collision batch and Euler step with the fused transport gather."""
+    two chunks and many; collision batch and Euler step with the fused transport gather; with the side-stream
+    transforms launched over sub-ranges of `sub` cells (FKS_PIPE_SUB; ragged last sub-range)."""
+    if sub is not None:
+        monkeypatch.setenv("FKS_PIPE_SUB", sub)
     cfg = CONFIGS["c3"]
     f = inputs.make_f(cfg, device=cuda_device, cells=list(range(n)))
     whole = make(cfg)
