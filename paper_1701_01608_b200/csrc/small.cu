@@ -560,11 +560,12 @@ fks_status small_prepare(Ctx& c) { return c.N == 16 ? small_prepare_n<16>(c) : s
 // summation order of G — hence every bit of Q — does not depend on how a batch is split into calls or chunks
 // Chunks of ~26 terms at N = 24 (c1: 10 chunks, 1920 units = 12.97 waves of the 148-CTA grid, so the last wave is
 // full: 3.672 ms per c1 step vs 3.729 with 32-term chunks (11.7 waves), 3.722 with 20 and 3.818 with 16;
-// profiles/r02_experiments.txt r2sc), ~8 terms at N = 16 (c0 has only 8 cells: parallelism over terms).
+// profiles/r02_experiments.txt r2sc), ~3 terms at N = 16 (c0 has only 8 cells: parallelism over terms; c0 step
+// 0.1275 ms with 8-term chunks (72 units), 0.1175 with 3 (144 units), 0.1245 with 2; r2c0).
 static int small_chunks(const Ctx& c) {
   const int T1 = c.T + 1;
   static const int tpc_env = [] { const char* e = std::getenv("FKS_SMALL_TPC"); return e ? std::atoi(e) : 0; }();
-  const int tpc = tpc_env > 0 ? tpc_env : (c.N == 24 ? 26 : 8);
+  const int tpc = tpc_env > 0 ? tpc_env : (c.N == 24 ? 26 : 3);
   return std::max(1, std::min(small_smax(), (T1 + tpc - 1) / tpc));
 }
 
